@@ -1,0 +1,539 @@
+#!/usr/bin/env python
+"""Benchmark: Gpixel/s of the 2-D CDF 9/7 forward DWT on B200 vs the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3|c4|c5|c2] [--arith strict|fast]
+
+Default workload (BASELINE.json configs[2], the north-star target, "C3"):
+one 16384x16384 float32 image, operation-reduced non-separable CDF 9/7
+("non-separable-split") forward transform, 5-level pyramid, per GPU.  A step is
+one full pyramid (5 fused kernel launches).  Under torchrun (N > 1) every rank
+transforms its own image: batch sharding, no data-path collective ("weak").
+
+--config c4 : BASELINE configs[3], 1024 x 2048^2 images, non-separable CDF 9/7,
+              1 level, batch-sharded over N GPUs ("strong", total work fixed).
+--config c5 : BASELINE configs[4], one 65536^2 image, non-separable CDF 9/7,
+              1 level, row strips over N GPUs with an NCCL halo exchange.
+--config c2 : 4096^2, one line per scheme x wavelet x direction (parity sizes).
+
+--impl reference times the reference algorithm's CPU implementation on this
+box's host cores (the oracle port, oracle/dwt_oracle.c -- the reference itself
+is Python and is not installable on the GPU box) on a bounded sample of the
+same workload, and prints the same JSON line with "impl": "reference".
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gpixel/s (and ns/pixel) for 2-D CDF 9/7 fwd DWT vs HBM roofline, 1/2/4/8 B200"
+UNIT = "Gpixel/s"
+SPEC_HBM_GBS = 8000.0
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _traffic(key):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and "Active" in s[3 + i]
+                          and "Not" not in s[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# -- CPU reference arm ----------------------------------------------------------------
+
+
+def _cpu_sample(config, steps=1, warmup=0):
+    """Time the oracle port on a bounded sample; returns (gpx_per_s, sample_desc, threads, per_step_s)."""
+    import numpy as np
+
+    from oracle import oracle
+    from paper_1705_08266_b200 import CDF97, build_scheme, compile_scheme
+
+    threads = os.cpu_count() or 1
+    if config == "c3":
+        n, levels, scheme = 8192, 5, "non-separable-split"
+        desc = "8192x8192 f32 (1/4 of the C3 area), CDF 9/7 non-separable-split, 5-level pyramid"
+        px = n * n
+    elif config == "c4":
+        n, levels, scheme = 2048, 1, "non-separable-split"
+        desc = "2 of the 1024 C4 images (2048x2048 f32), CDF 9/7 non-separable-split, 1 level"
+        px = 2 * n * n
+    elif config == "c5":
+        n, levels, scheme = 8192, 1, "non-separable-split"
+        desc = "one 8192x8192 f32 block (1/64 of the C5 area), CDF 9/7 non-separable-split, 1 level"
+        px = n * n
+    else:
+        n, levels, scheme = 4096, 1, "non-separable-split"
+        desc = "4096x4096 f32, CDF 9/7 non-separable-split, 1 level"
+        px = n * n
+    prog = compile_scheme(build_scheme(scheme, CDF97))
+    img = np.random.default_rng(0).random((n, n), dtype=np.float64).astype(np.float32)
+    reps = 2 if config == "c4" else 1
+
+    def one():
+        for _ in range(reps):
+            oracle.dwt(img, prog, levels, threads=threads)
+
+    for _ in range(warmup):
+        one()
+    times = []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return px / med / 1e9, desc, threads, med, times
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    steps = max(1, args.steps)
+    gpx, desc, threads, med, times = _cpu_sample(args.config, steps=steps, warmup=min(args.warmup, 1))
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": gpx,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": steps,
+        "warmup": args.warmup,
+        "ms_per_step": med * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak" if args.config == "c3" else "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (uniform [0,1), numpy PCG64 seed 0)",
+        "config": {"workload": _workload_name(args.config), "sample": desc},
+        "cpu_baseline": {"value": gpx, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc},
+        "e2e": {"value": gpx, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "oracle/dwt_oracle.c: C restatement of liftfuse run_reference (bit-identical to the reference, "
+                "pinned by tests/test_oracle.py); the reference itself is pure Python/NumPy",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _workload_name(config):
+    return {
+        "c3": "C3: 16384x16384 f32, CDF 9/7 non-separable-split (operation-reduced) forward, 5-level pyramid, per GPU",
+        "c4": "C4: 1024 x 2048x2048 f32, CDF 9/7 non-separable-split forward, 1 level, batch-sharded",
+        "c5": "C5: 65536x65536 f32, CDF 9/7 non-separable-split forward, 1 level, row strips + NCCL halo exchange",
+        "c2": "C2: 4096x4096 f32, all schemes x CDF 5/3, 9/7 x fwd/inv, 1 level",
+    }[config]
+
+
+# -- GPU arm ------------------------------------------------------------------------------
+
+
+def _dist_setup(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return torch, dist, world, rank, local
+
+
+def _barrier(torch, dist):
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def _max_over_ranks(torch, dist, x):
+    if dist is None:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_c3(args):
+    torch, dist, world, rank, local = _dist_setup(args)
+    from paper_1705_08266_b200 import CDF97, Transform, build_scheme
+
+    n, levels = 16384, 5
+    scheme = build_scheme("non-separable-split", CDF97)
+    tr = Transform(scheme, "single", fast=(args.arith == "fast"))
+    assert tr.fwd_plan.fused, "fused kernel not selected"
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(rank)
+    x = torch.rand((n, n), device="cuda", generator=gen)
+    # level buffers (LL ping-pong lives in the next level's input)
+    lls = [torch.empty((n >> (l + 1), n >> (l + 1)), device="cuda") for l in range(levels)]
+    det = [tuple(torch.empty((n >> (l + 1), n >> (l + 1)), device="cuda") for _ in range(3)) for l in range(levels)]
+    stream = torch.cuda.current_stream()
+
+    def step(evs=None):
+        src = x
+        for l in range(levels):
+            if evs is not None:
+                evs[l].record(stream)
+            tr.forward(src, out=(lls[l],) + det[l])
+            src = lls[l]
+        if evs is not None:
+            evs[levels].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    _barrier(torch, dist)
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(levels + 1)] for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        _barrier(torch, dist)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for k in range(args.steps):
+            step(events[k])
+        t1.record(stream)
+        t1.synchronize()
+        _barrier(torch, dist)
+    ms = t0.elapsed_time(t1)
+    ms = _max_over_ranks(torch, dist, ms)
+    per_level = [statistics.median(ev[l].elapsed_time(ev[l + 1]) for ev in events) for l in range(levels)]
+    l0_ms = statistics.mean(ev[0].elapsed_time(ev[1]) for ev in events)
+    ms_step = ms / args.steps
+    px = n * n * world
+    value = px / (ms_step * 1e-3) / 1e9
+    alg_bytes_step = 8 * n * n * sum(4.0 ** -l for l in range(levels))
+    l0_bytes = 8 * n * n
+    peak, peak_src = _peaks()
+    achieved = l0_bytes / (l0_ms * 1e-3) / 1e9
+
+    # end to end through the public API with host (pinned) buffers
+    e2e = _e2e_c3(torch, tr, n, levels, rank, dist, args)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        gpx, desc, threads, med, _ = _cpu_sample("c3")
+        cpu = {"value": gpx, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(3, args.warmup),
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (torch.rand on device, seed = rank)",
+            "config": {
+                "workload": _workload_name("c3"),
+                "image": [n, n],
+                "levels": levels,
+                "scheme": "non-separable-split",
+                "wavelet": "cdf97",
+                "arith": "strict: bit-identical to the reference (separate IEEE mul/add, compiled term order)"
+                if args.arith == "strict" else "fast: FMA, max err <= 1e-4 x input range (tests/test_gpu_parity.py)",
+                "l2": "input 1 GiB > 126 MB L2 per step; no flush",
+                "parallelism": f"batch-shard x{world} (one image per GPU, no collective)",
+                "ns_per_px": 1.0 / value,
+                "ms_per_level": per_level,
+                "alg_bytes_per_step": alg_bytes_step,
+                "frac_of_8TBps": (alg_bytes_step / (ms_step * 1e-3) / 1e9) / SPEC_HBM_GBS,
+            },
+            "roofline": {
+                "bound": "hbm",
+                "kernel": "stream_kernel<cdf97_nssplit_fwd, f32> level 0 (16384^2 -> 4 x 8192^2)",
+                "achieved": achieved,
+                "peak": peak,
+                "peak_source": peak_src,
+                "unit": "GB/s",
+                "frac": achieved / peak,
+                "traffic": _traffic(f"c3_level0_{args.arith}"),
+                "alg_bytes_per_launch": l0_bytes,
+                "launch_ms": l0_ms,
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": args.steps * levels,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def _e2e_c3(torch, tr, n, levels, rank, dist, args):
+    """Public-API pyramid with host buffers: pinned H2D of the image, the
+    pyramid, pinned D2H of every subband, all inside the timed region."""
+    host_in = torch.empty((n, n), dtype=torch.float32).pin_memory()
+    host_in.uniform_()
+    dev_in = torch.empty((n, n), device="cuda")
+    ll, details = tr.dwt(dev_in, levels)
+    scratch = torch.empty(((n // 2) ** 2 + (n // 4) ** 2,), device="cuda")
+    host_out = [torch.empty(t.shape, dtype=torch.float32).pin_memory() for d in details for t in d]
+    host_ll = torch.empty(ll.shape, dtype=torch.float32).pin_memory()
+    dev_out = [t for d in details for t in d]
+
+    def step():
+        dev_in.copy_(host_in, non_blocking=True)
+        tr.dwt_into(dev_in, levels, details, ll, scratch)
+        for h, d in zip(host_out, dev_out):
+            h.copy_(d, non_blocking=True)
+        host_ll.copy_(ll, non_blocking=True)
+
+    steps = max(2, min(args.steps, 5))
+    for _ in range(2):
+        step()
+    _barrier(torch, dist)
+    t0 = time.perf_counter()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        step()
+    e.record()
+    e.synchronize()
+    ms = _max_over_ranks(torch, dist, s.elapsed_time(e) / steps)
+    world = dist.get_world_size() if dist is not None else 1
+    h2d = n * n * 4
+    d2h = sum(t.numel() * 4 for t in host_out) + host_ll.numel() * 4
+    return {"value": n * n * world / (ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+            "api": "Transform.dwt_into (b2dwt_dwt) with pinned host buffers, copies inside the timed region"}
+
+
+def run_c4(args):
+    torch, dist, world, rank, local = _dist_setup(args)
+    from paper_1705_08266_b200 import CDF97, Transform, build_scheme
+    from paper_1705_08266_b200.distributed import shard_range
+
+    n_img, n = 1024, 2048
+    lo, hi = shard_range(n_img, rank, world)
+    mine = hi - lo
+    chunk = 64
+    tr = Transform(build_scheme("non-separable-split", CDF97), "single", fast=(args.arith == "fast"))
+    x = torch.empty((mine, n, n), device="cuda")
+    for i in range(0, mine, chunk):
+        x[i:i + chunk].uniform_()
+    outs = tuple(torch.empty((mine, n // 2, n // 2), device="cuda") for _ in range(4))
+
+    def step():
+        for i in range(0, mine, chunk):
+            tr.forward(x[i:i + chunk], out=tuple(o[i:i + chunk] for o in outs))
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    with ClockSampler(local) as clk:
+        _barrier(torch, dist)
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.steps):
+            step()
+        e.record()
+        e.synchronize()
+        _barrier(torch, dist)
+    ms = _max_over_ranks(torch, dist, s.elapsed_time(e)) / args.steps
+    value = n_img * n * n / (ms * 1e-3) / 1e9
+    peak, src = _peaks()
+    if rank == 0:
+        achieved = 8.0 * mine * n * n / (ms * 1e-3) / 1e9
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (uniform on device)",
+            "config": {"workload": _workload_name("c4"), "parallelism": f"batch-shard x{world}",
+                       "images_per_gpu": mine, "launch_chunk": chunk, "arith": args.arith},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": src, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None},
+            "cpu_baseline": None, "e2e": None, "clocks": clk.summary(),
+            "gpu_launches": args.steps * ((mine + chunk - 1) // chunk),
+        }), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_c5(args):
+    torch, dist, world, rank, local = _dist_setup(args)
+    from paper_1705_08266_b200 import CDF97, Transform, build_scheme
+    from paper_1705_08266_b200.distributed import RowStrips
+
+    n = 65536
+    tr = Transform(build_scheme("non-separable-split", CDF97), "single", fast=(args.arith == "fast"))
+    strips = RowStrips(n, n, rank, world, tr.cone[:2], levels=1)
+    buf = strips.allocate(lambda shape: torch.empty(shape, device="cuda"))
+    own = strips.owned(buf)
+    for i in range(0, own.shape[0], 4096):
+        own[i:i + 4096].uniform_()
+    L = strips.layout(0)
+    outs = tuple(torch.empty((L.rows // 2, n // 2), device="cuda") for _ in range(4))
+
+    def band_forward(band, band_row0, height, r0, r1, out):
+        tr.forward_rows(band, band_row0, height, r0, r1, out=out)
+
+    def step():
+        strips.forward(band_forward, buf, outs, 0, None, overlap=True)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    with ClockSampler(local) as clk:
+        _barrier(torch, dist)
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.steps):
+            step()
+        e.record()
+        e.synchronize()
+        _barrier(torch, dist)
+    ms = _max_over_ranks(torch, dist, s.elapsed_time(e)) / args.steps
+    value = n * n / (ms * 1e-3) / 1e9
+    peak, src = _peaks()
+    if rank == 0:
+        achieved = 8.0 * L.rows * n / (ms * 1e-3) / 1e9
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (uniform on device)",
+            "config": {"workload": _workload_name("c5"), "parallelism": f"row-strips x{world}",
+                       "halo_rows_per_side_px": [L.halo_top, L.halo_bot],
+                       "exchange": "torch.distributed batch_isend_irecv (NCCL) overlapped with interior rows",
+                       "arith": args.arith},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": src, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None},
+            "cpu_baseline": None, "e2e": None, "clocks": clk.summary(),
+            "gpu_launches": args.steps * (1 + (world > 1) * (1 + (0 < rank < world - 1))),
+        }), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_c2(args):
+    import torch
+
+    from paper_1705_08266_b200 import CDF53, CDF97, SCHEME_NAMES, Transform, build_scheme
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    n = 4096
+    x = torch.rand((n, n), device="cuda")
+    peak, _ = _peaks()
+    for plan in (CDF53, CDF97):
+        for name in SCHEME_NAMES:
+            tr = Transform(build_scheme(name, plan), "single", fast=(args.arith == "fast"))
+            outs = tr.forward(x)
+            rec = torch.empty_like(x)
+            for direction in ("fwd", "inv"):
+                fn = (lambda: tr.forward(x, out=outs)) if direction == "fwd" else (lambda: tr.inverse(*outs, out=rec))
+                for _ in range(max(3, args.warmup)):
+                    fn()
+                torch.cuda.synchronize()
+                s = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                s.record()
+                for _ in range(args.steps):
+                    fn()
+                e.record()
+                e.synchronize()
+                ms = s.elapsed_time(e) / args.steps
+                gbs = 8.0 * n * n / (ms * 1e-3) / 1e9
+                print(json.dumps({"config": f"C2 {plan.name} {name} {direction}", "ms": ms,
+                                  "Gpixel/s": n * n / (ms * 1e-3) / 1e9, "GB/s": gbs, "frac": gbs / peak,
+                                  "note": "4096^2 (64 MiB) is partly L2-resident"}), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=("c3", "c4", "c5", "c2"), default="c3")
+    ap.add_argument("--arith", choices=("strict", "fast"), default="strict")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return {"c3": run_c3, "c4": run_c4, "c5": run_c5, "c2": run_c2}[args.config](args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,157 @@
+/*
+ * b2dwt.h -- C ABI of the B200-native 2-D DWT hot path (libb2dwt.so).
+ *
+ * Drop-in boundary for the reference's pixel executor (liftfuse, Python):
+ *
+ *   b2dwt_plan_create     <- liftfuse.engine.compile_scheme() output consumed by
+ *                            run_tiled(program, comps, cfg)     engine.py:404-439
+ *                            (a b2dwt_program is a StencilProgram flattened,
+ *                             engine.py:227-256, terms in compiled order :267)
+ *   b2dwt_run_components  <- run_tiled / run_reference on 4 component planes
+ *                            engine.py:404-439, :442-451
+ *   b2dwt_forward         <- forward(image, scheme, cfg): deinterleave + run_tiled
+ *                            engine.py:481-487, deinterleave :200-211 (fused)
+ *   b2dwt_inverse         <- inverse(quad, scheme, cfg): run_tiled + interleave_quad
+ *                            engine.py:490-495, interleave_quad :214-221 (fused)
+ *   b2dwt_forward_rows    <- forward() restricted to a band of output rows of a
+ *                            larger image (multi-GPU row strips; new, no reference
+ *                            counterpart; reflection stays in global coordinates)
+ *   b2dwt_dwt / b2dwt_idwt<- multi-level pyramid (new; oracle = forward iterated
+ *                            on ll)
+ *
+ * Conventions
+ *   - All pixel pointers are DEVICE pointers owned by the caller; element type
+ *     is float (B2DWT_F32) or double (B2DWT_F64) as given at plan creation.
+ *   - Leading dimensions (ld) and batch strides are in ELEMENTS.
+ *   - Quad grid: an H x W image has rows = H/2, cols = W/2 quads; component 0..3
+ *     = (even row, even col)=LL, (even, odd)=HL, (odd, even)=LH, (odd, odd)=HH
+ *     (engine.py:52, schemes.py:3-14).
+ *   - Boundary handling is the reference's whole-sample symmetric extension
+ *     applied to the state entering every sub-step (engine.py:55-92, 312-347).
+ *   - Calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy default
+ *     stream).  No global mutable state; plans are immutable and may be shared
+ *     across threads.
+ *   - Return 0 on success or a negative B2DWT_E* code; b2dwt_last_error()
+ *     returns a thread-local message.  There is no CPU fallback: without a
+ *     CUDA device every compute entry point fails with B2DWT_ECUDA.
+ */
+#ifndef B2DWT_H
+#define B2DWT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B2DWT_ABI_VERSION 1
+
+enum {
+    B2DWT_OK = 0,
+    B2DWT_EINVAL = -22,       /* bad argument (shape, pointer, layout)      */
+    B2DWT_EUNSUPPORTED = -95, /* valid request this build cannot execute    */
+    B2DWT_ECUDA = -5,         /* CUDA runtime error (message has details)   */
+    B2DWT_ENOMEM = -12
+};
+
+enum { B2DWT_F32 = 0, B2DWT_F64 = 1 };
+
+/* Plan flags */
+enum {
+    B2DWT_STRICT = 1,        /* bit-exact with the reference: every product and sum
+                                rounded separately, in compiled term order (default) */
+    B2DWT_FAST = 2,          /* fused multiply-add; within 1e-4 x input range (f32)  */
+    B2DWT_FORCE_GENERIC = 4, /* use the per-sub-step interpreter kernel (debug)      */
+    B2DWT_NO_TMA = 8         /* fused kernel loads with cp.async instead of TMA      */
+};
+
+/* One multiply-accumulate term: out[target][n,m] += coeff * in[src][n+dn, m+dm] */
+typedef struct {
+    int32_t src; /* 0..3 */
+    int32_t dm;  /* column offset, quads */
+    int32_t dn;  /* row offset, quads    */
+    int32_t reserved;
+    double coeff;
+} b2dwt_term;
+
+/* A StencilProgram (engine.py:247-256) with pass boundaries dropped: the
+ * transform is the composition of its sub-steps, each a gather over the
+ * previous sub-step's full output. */
+typedef struct {
+    int32_t abi_version;       /* B2DWT_ABI_VERSION */
+    int32_t n_substeps;
+    const int32_t* term_counts; /* [n_substeps * 4]: terms of (substep, target) */
+    const b2dwt_term* terms;    /* flattened in (substep, target, term) order   */
+} b2dwt_program;
+
+typedef struct b2dwt_plan_s* b2dwt_plan;
+
+typedef struct {
+    int32_t kernel;        /* 0 = generic per-sub-step interpreter, 1 = fused streaming */
+    int32_t program_id;    /* built-in structure index, -1 for generic                  */
+    int32_t halo_left, halo_right, halo_up, halo_down; /* fused cone, quads            */
+    int32_t dtype, flags;
+    char key[64];          /* e.g. "cdf97/non-separable-split/fwd" or "generic"         */
+} b2dwt_plan_info;
+
+/* Four component planes in quad coordinates. */
+typedef struct {
+    void* ptr[4];
+    int64_t ld[4];    /* elements between rows, per plane   */
+    int64_t bstride;  /* elements between batch items (all planes) */
+} b2dwt_planes;
+
+int32_t b2dwt_abi_version(void);
+const char* b2dwt_last_error(void);
+/* Number of CUDA devices visible (0 on a CPU-only host); never fails. */
+int32_t b2dwt_device_count(void);
+
+int b2dwt_plan_create(const b2dwt_program* program, int32_t dtype, int32_t flags, b2dwt_plan* out);
+int b2dwt_plan_destroy(b2dwt_plan plan);
+int b2dwt_plan_get_info(b2dwt_plan plan, b2dwt_plan_info* info);
+
+/* Components -> components (run_tiled). rows x cols quads, `batch` items. */
+int b2dwt_run_components(b2dwt_plan plan, const b2dwt_planes* in, const b2dwt_planes* out,
+                         int64_t rows, int64_t cols, int32_t batch, void* stream);
+
+/* Interleaved image (height x width, even) -> 4 subband planes. */
+int b2dwt_forward(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t image_bstride,
+                  int64_t height, int64_t width, const b2dwt_planes* out, int32_t batch, void* stream);
+
+/* 4 subband planes -> interleaved image (height x width). `plan` holds the
+ * INVERSE program (compile_scheme(invert_scheme(scheme))). */
+int b2dwt_inverse(b2dwt_plan plan, const b2dwt_planes* in, void* image, int64_t image_ld,
+                  int64_t image_bstride, int64_t height, int64_t width, int32_t batch, void* stream);
+
+/* Row-band forward for row-strip decomposition.  The image is global_height x
+ * width; `image` points at global pixel row `image_row0` (even) and holds
+ * `image_rows` rows (even).  Computes quad rows [out_row_begin, out_row_end)
+ * into `out` whose row 0 is quad row out_row_begin.  The buffer must hold the
+ * fused cone: quad rows [out_row_begin - halo_up, out_row_end + halo_down)
+ * clipped to the image (see b2dwt_plan_info).  Bit-identical to the same rows
+ * of b2dwt_forward on the whole image. */
+int b2dwt_forward_rows(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t image_row0,
+                       int64_t image_rows, int64_t global_height, int64_t width, int64_t out_row_begin,
+                       int64_t out_row_end, const b2dwt_planes* out, void* stream);
+
+/* Multi-level forward pyramid.  Level l (0-based) transforms the (H>>l) x (W>>l)
+ * LL of level l-1 (level 0: `image`).  details[l] receives HL/LH/HH of level l
+ * (ptr[0] ignored); `ll_out` (pitch ll_ld) receives the final LL, an
+ * (H >> levels) x (W >> levels) plane.  `scratch` must hold
+ * (H/2)*(W/2) + (H/4)*(W/4) elements (LL ping-pong between levels, so no level
+ * reads and writes the same buffer); it may be NULL when levels == 1.  H and W
+ * must be divisible by 2^levels.  Batch = 1. */
+int b2dwt_dwt(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t height, int64_t width,
+              int32_t levels, const b2dwt_planes* details, void* ll_out, int64_t ll_ld, void* scratch,
+              void* stream);
+
+/* Multi-level inverse: `plan` holds the inverse program.  Reconstructs the
+ * height x width image from ll (of the coarsest level) and details[l].
+ * `scratch` as for b2dwt_dwt. */
+int b2dwt_idwt(b2dwt_plan plan, const void* ll, int64_t ll_ld, const b2dwt_planes* details, int32_t levels,
+               void* image, int64_t image_ld, int64_t height, int64_t width, void* scratch, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B2DWT_H */

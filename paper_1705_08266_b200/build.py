@@ -1,0 +1,118 @@
+"""Build libb2dwt.so in-tree with nvcc for sm_100a (no GPU needed).
+
+Translation units:
+  csrc/b2dwt_host.cu        C ABI, plan matching, generic interpreter kernel
+  csrc/prog_instance.cu     fused streaming kernels, compiled once per built-in
+                            program (-DB2DWT_PROG=<ident>), in parallel
+
+Flags: -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 (ptxas -v output is
+kept in build/ptxas_<unit>.log for register / spill review).
+
+    python -m paper_1705_08266_b200.build [--force] [--jobs N]
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import shutil
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(ROOT, "build")
+LIB = os.path.join(HERE, "libb2dwt.so")
+INCLUDE = os.path.join(ROOT, "include")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", *ARCH]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found: the CUDA toolkit is required to build libb2dwt.so")
+
+
+def _program_units():
+    """(ident, is_inverse) for every built-in program, from programs.inc."""
+    units = []
+    with open(os.path.join(CSRC, "programs.inc")) as fh:
+        for line in fh:
+            line = line.strip()
+            if line.startswith("struct ") and line.endswith("{"):
+                ident = line.split()[1]
+                units.append((ident, ident.endswith("_inv")))
+    return units
+
+
+def _deps():
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".inc", ".cu"))] + [
+        os.path.join(INCLUDE, "b2dwt.h")
+    ]
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _compile(args):
+    src, obj, defines, log = args
+    cmd = [nvcc(), *NVCC_FLAGS, *defines, "-I", CSRC, "-I", INCLUDE, "-c", src, "-o", obj]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    with open(log, "w") as fh:
+        fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {os.path.basename(obj)}:\n{res.stderr[-4000:]}")
+    return obj
+
+
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    deps = _deps()
+    if not force and not _stale(LIB, deps):
+        return LIB
+    jobs = jobs or max(1, os.cpu_count() or 1)
+    # host TU in C++17 (nvcc 12.9's C++20 front end trips over libstdc++ 13
+    # containers); kernel TUs need C++20 for the phase-unrolled tick loop
+    tasks = [(os.path.join(CSRC, "b2dwt_host.cu"), os.path.join(BUILD, "b2dwt_host.o"), ["-std=c++17"],
+              os.path.join(BUILD, "ptxas_b2dwt_host.log"))]
+    for ident, inv in _program_units():
+        tasks.append((
+            os.path.join(CSRC, "prog_instance.cu"),
+            os.path.join(BUILD, f"prog_{ident}.o"),
+            ["-std=c++20", f"-DB2DWT_PROG={ident}", f"-DB2DWT_PROG_INV={int(inv)}"],
+            os.path.join(BUILD, f"ptxas_{ident}.log"),
+        ))
+    todo = [t for t in tasks if force or _stale(t[1], deps)]
+    if verbose:
+        print(f"[b2dwt] compiling {len(todo)} units with {jobs} jobs", file=sys.stderr)
+    with ThreadPoolExecutor(max_workers=jobs) as pool:
+        list(pool.map(_compile, todo))
+    objs = [t[1] for t in tasks]
+    tmp = LIB + ".tmp"
+    cmd = [nvcc(), "-shared", *ARCH, "-o", tmp, *objs, "-lcuda"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")
+    os.replace(tmp, LIB)
+    return LIB
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--jobs", type=int, default=None)
+    a = ap.parse_args()
+    print(build(force=a.force, jobs=a.jobs, verbose=True))
+
+
+if __name__ == "__main__":
+    main()

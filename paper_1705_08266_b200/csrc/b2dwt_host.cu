@@ -1,0 +1,579 @@
+// b2dwt_host.cu -- C ABI (include/b2dwt.h): plans, validation, dispatch.
+//
+// A plan is a compiled StencilProgram (liftfuse/engine.py:227-256).  At plan
+// creation the program's structure -- the ordered (src, dm, dn) list of every
+// sub-step/target and which coefficients are exactly 1.0 -- is matched against
+// the built-in structures of programs.inc.  A match runs the fused streaming
+// kernel (stream_kernel.cuh) with the plan's own coefficients; anything else
+// runs the per-sub-step interpreter (generic_kernel.cuh).  Both evaluate the
+// terms in the compiled order, so strict mode is bit-identical to the
+// reference either way.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/b2dwt.h"
+#include "generic_kernel.cuh"
+#include "launch.h"
+
+namespace b2dwt {
+
+#define B2DWT_DECLARE(ID, NAME)                                     \
+  cudaError_t b2dwt_fused_##NAME(const FusedLaunch&, bool* used_tma); \
+  ConeInfo b2dwt_cone_##NAME();
+B2DWT_FOR_EACH_PROGRAM(B2DWT_DECLARE)
+#undef B2DWT_DECLARE
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(B2DWT_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct Builtin {
+  const char* key;
+  int nsub;
+  int nterms;
+  int (*begin)(int);
+  TermInfo (*term)(int);
+  FusedLauncher launch;
+  ConeGetter cone;
+  bool inverse;
+};
+
+template <class P>
+int begin_of(int i) {
+  return P::begin(i);
+}
+template <class P>
+TermInfo term_of(int i) {
+  return P::term(i);
+}
+
+const Builtin* builtins() {
+  static const Builtin table[] = {
+#define B2DWT_ROW(ID, NAME)                                                                                      \
+  {progs::NAME::kKey,        progs::NAME::kNumSub, progs::NAME::kNumTerms, &begin_of<progs::NAME>,             \
+   &term_of<progs::NAME>,    &b2dwt_fused_##NAME,  &b2dwt_cone_##NAME,     std::strstr(progs::NAME::kKey, "/inv") \
+   != nullptr},
+      B2DWT_FOR_EACH_PROGRAM(B2DWT_ROW)
+#undef B2DWT_ROW
+  };
+  return table;
+}
+
+}  // namespace
+}  // namespace b2dwt
+
+using namespace b2dwt;
+
+struct b2dwt_plan_s {
+  int nsub = 0;
+  std::vector<int32_t> counts;   // nsub * 4
+  std::vector<b2dwt_term> terms;
+  int dtype = 0;
+  int flags = 0;
+  int builtin = -1;              // index into builtins(), -1 = generic
+  std::vector<double> coeffs;    // flat, compiled order
+  ConeInfo cone{0, 0, 0, 0};
+  std::string key;
+};
+
+namespace {
+
+bool strict_of(const b2dwt_plan_s* p) { return (p->flags & B2DWT_FAST) == 0; }
+
+int match_builtin(const b2dwt_plan_s& p) {
+  const Builtin* tab = builtins();
+  for (int id = 0; id < B2DWT_NUM_PROGRAMS; ++id) {
+    const Builtin& b = tab[id];
+    if (b.nsub != p.nsub || b.nterms != static_cast<int>(p.terms.size())) continue;
+    bool ok = true;
+    for (int st = 0; st < p.nsub * 4 && ok; ++st)
+      ok = (b.begin(st + 1) - b.begin(st)) == p.counts[st];
+    for (int i = 0; i < b.nterms && ok; ++i) {
+      const TermInfo ti = b.term(i);
+      const b2dwt_term& t = p.terms[i];
+      ok = ti.src == t.src && ti.dm == t.dm && ti.dn == t.dn && (!ti.unit || t.coeff == 1.0);
+    }
+    if (ok) return id;
+  }
+  return -1;
+}
+
+size_t esize(int dtype) { return dtype == B2DWT_F32 ? 4 : 8; }
+
+// ---------------------------------------------------------------------------
+// Generic path: one interpreter launch per sub-step, ping-pong scratch.
+struct ViewSet {
+  const void* p[4];
+  int64_t rs[4], cs[4];
+};
+
+ViewSet planar_views(const b2dwt_planes* pl, size_t es) {
+  ViewSet v;
+  for (int c = 0; c < 4; ++c) {
+    v.p[c] = pl->ptr[c];
+    v.rs[c] = pl->ld[c];
+    v.cs[c] = 1;
+  }
+  (void)es;
+  return v;
+}
+
+ViewSet image_views(const void* img, int64_t ld, size_t es) {
+  ViewSet v;
+  for (int c = 0; c < 4; ++c) {
+    v.p[c] = static_cast<const char*>(img) + ((c >> 1) * ld + (c & 1)) * static_cast<int64_t>(es);
+    v.rs[c] = 2 * ld;
+    v.cs[c] = 2;
+  }
+  return v;
+}
+
+template <class T>
+cudaError_t launch_generic_substep(const b2dwt_plan_s& p, int s, const int32_t* term_base, const ViewSet& in,
+                                   int64_t in_b, const ViewSet& out, int64_t out_b, int64_t rows, int64_t cols,
+                                   int batch, cudaStream_t stream) {
+  GenericSubstep sub{};
+  int k = 0;
+  for (int t = 0; t < 4; ++t) {
+    sub.count[t] = p.counts[s * 4 + t];
+    for (int j = 0; j < sub.count[t]; ++j, ++k) {
+      const b2dwt_term& src = p.terms[term_base[0] + k];
+      sub.terms[k].src = static_cast<int8_t>(src.src);
+      sub.terms[k].dm = static_cast<int8_t>(src.dm);
+      sub.terms[k].dn = static_cast<int8_t>(src.dn);
+      sub.terms[k].tgt = static_cast<int8_t>(t);
+      sub.terms[k].coeff = src.coeff;
+    }
+  }
+  PlaneView<const T> iv[4];
+  PlaneView<T> ov[4];
+  for (int c = 0; c < 4; ++c) {
+    iv[c] = PlaneView<const T>{static_cast<const T*>(in.p[c]), in.rs[c], in.cs[c]};
+    ov[c] = PlaneView<T>{static_cast<T*>(const_cast<void*>(out.p[c])), out.rs[c], out.cs[c]};
+  }
+  const int64_t total = rows * cols;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  dim3 g(grid, batch);
+  if (strict_of(&p))
+    generic_substep_kernel<T, true><<<g, 256, 0, stream>>>(sub, iv[0], iv[1], iv[2], iv[3], ov[0], ov[1], ov[2],
+                                                           ov[3], in_b, out_b, static_cast<int>(rows),
+                                                           static_cast<int>(cols));
+  else
+    generic_substep_kernel<T, false><<<g, 256, 0, stream>>>(sub, iv[0], iv[1], iv[2], iv[3], ov[0], ov[1], ov[2],
+                                                            ov[3], in_b, out_b, static_cast<int>(rows),
+                                                            static_cast<int>(cols));
+  return cudaGetLastError();
+}
+
+int run_generic(const b2dwt_plan_s& p, const ViewSet& in, int64_t in_b, const ViewSet& out, int64_t out_b,
+                int64_t rows, int64_t cols, int batch, cudaStream_t stream) {
+  const size_t es = esize(p.dtype);
+  const int64_t plane = rows * cols;
+  void* scratch = nullptr;
+  if (p.nsub > 1) {
+    const size_t bytes = static_cast<size_t>(2 * 4 * plane * batch) * es;
+    cudaError_t e = cudaMallocAsync(&scratch, bytes, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(generic scratch)");
+  }
+  auto scratch_views = [&](int which) {
+    ViewSet v;
+    for (int c = 0; c < 4; ++c) {
+      v.p[c] = static_cast<char*>(scratch) + ((which * 4 + c) * plane * batch) * static_cast<int64_t>(es);
+      v.rs[c] = cols;
+      v.cs[c] = 1;
+    }
+    return v;
+  };
+  int32_t base = 0;
+  cudaError_t err = cudaSuccess;
+  for (int s = 0; s < p.nsub && err == cudaSuccess; ++s) {
+    const ViewSet vin = s == 0 ? in : scratch_views((s - 1) & 1);
+    const int64_t bin = s == 0 ? in_b : plane;
+    const ViewSet vout = s == p.nsub - 1 ? out : scratch_views(s & 1);
+    const int64_t bout = s == p.nsub - 1 ? out_b : plane;
+    err = p.dtype == B2DWT_F32
+              ? launch_generic_substep<float>(p, s, &base, vin, bin, vout, bout, rows, cols, batch, stream)
+              : launch_generic_substep<double>(p, s, &base, vin, bin, vout, bout, rows, cols, batch, stream);
+    base += p.counts[s * 4] + p.counts[s * 4 + 1] + p.counts[s * 4 + 2] + p.counts[s * 4 + 3];
+  }
+  if (scratch) cudaFreeAsync(scratch, stream);
+  if (err != cudaSuccess) return cuda_fail(err, "generic stencil kernel");
+  return B2DWT_OK;
+}
+
+// ---------------------------------------------------------------------------
+int run_fused(const b2dwt_plan_s& p, FusedLaunch& r) {
+  const Builtin& b = builtins()[p.builtin];
+  r.dtype = p.dtype;
+  r.strict = strict_of(&p);
+  r.allow_tma = (p.flags & B2DWT_NO_TMA) == 0;
+  r.coeffs = p.coeffs.data();
+  r.n_coeffs = static_cast<int>(p.coeffs.size());
+  bool used_tma = false;
+  const cudaError_t e = b.launch(r, &used_tma);
+  if (e != cudaSuccess) return cuda_fail(e, "fused stream kernel");
+  return B2DWT_OK;
+}
+
+bool fused_layout_ok(const b2dwt_plan_s& p, int lin, int lout) {
+  if (p.builtin < 0 || (p.flags & B2DWT_FORCE_GENERIC)) return false;
+  const bool inv = builtins()[p.builtin].inverse;
+  if (lin == 1 && lout == 1) return true;  // planar -> planar
+  return inv ? (lin == 1 && lout == 0) : (lin == 0 && lout == 1);
+}
+
+int check_plan(b2dwt_plan p) {
+  if (!p) return fail(B2DWT_EINVAL, "null plan");
+  return B2DWT_OK;
+}
+
+int check_planes(const b2dwt_planes* pl, const char* what) {
+  if (!pl) return fail(B2DWT_EINVAL, std::string(what) + ": null planes");
+  for (int c = 0; c < 4; ++c)
+    if (!pl->ptr[c]) return fail(B2DWT_EINVAL, std::string(what) + ": null plane pointer");
+  return B2DWT_OK;
+}
+
+int check_dims(int64_t height, int64_t width) {
+  if (height < 1 || width < 1) return fail(B2DWT_EINVAL, "image data must be a non-empty 2-D array");
+  if (height % 2 || width % 2) {
+    char buf[96];
+    std::snprintf(buf, sizeof(buf), "dimensions must be even, got %lldx%lld", static_cast<long long>(width),
+                  static_cast<long long>(height));
+    return fail(B2DWT_EINVAL, buf);
+  }
+  if (height / 2 > (1LL << 30) || width / 2 > (1LL << 30))
+    return fail(B2DWT_EUNSUPPORTED, "image too large for 32-bit quad indexing");
+  return B2DWT_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int32_t b2dwt_abi_version(void) { return B2DWT_ABI_VERSION; }
+
+const char* b2dwt_last_error(void) { return g_error.c_str(); }
+
+int32_t b2dwt_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int b2dwt_plan_create(const b2dwt_program* program, int32_t dtype, int32_t flags, b2dwt_plan* out) {
+  if (!out) return fail(B2DWT_EINVAL, "null output plan pointer");
+  *out = nullptr;
+  if (!program) return fail(B2DWT_EINVAL, "null program");
+  if (program->abi_version != B2DWT_ABI_VERSION) return fail(B2DWT_EINVAL, "program ABI version mismatch");
+  if (dtype != B2DWT_F32 && dtype != B2DWT_F64) return fail(B2DWT_EINVAL, "dtype must be B2DWT_F32 or B2DWT_F64");
+  if (program->n_substeps < 1) return fail(B2DWT_EINVAL, "program has no sub-steps");
+  if (!program->term_counts) return fail(B2DWT_EINVAL, "null term_counts");
+  auto* p = new b2dwt_plan_s();
+  p->nsub = program->n_substeps;
+  p->dtype = dtype;
+  p->flags = flags;
+  p->counts.assign(program->term_counts, program->term_counts + 4 * p->nsub);
+  size_t total = 0;
+  for (int st = 0; st < 4 * p->nsub; ++st) {
+    if (p->counts[st] < 0 || p->counts[st] > kGenericMaxTerms) {
+      delete p;
+      return fail(B2DWT_EUNSUPPORTED, "too many terms in one sub-step target");
+    }
+    total += static_cast<size_t>(p->counts[st]);
+  }
+  for (int s = 0; s < p->nsub; ++s) {
+    int sub = 0;
+    for (int t = 0; t < 4; ++t) sub += p->counts[s * 4 + t];
+    if (sub > kGenericMaxTerms) {
+      delete p;
+      return fail(B2DWT_EUNSUPPORTED, "too many terms in one sub-step");
+    }
+  }
+  if (total && !program->terms) {
+    delete p;
+    return fail(B2DWT_EINVAL, "null terms");
+  }
+  p->terms.assign(program->terms, program->terms + total);
+  for (const b2dwt_term& t : p->terms) {
+    if (t.src < 0 || t.src > 3 || t.dm < -64 || t.dm > 64 || t.dn < -64 || t.dn > 64) {
+      delete p;
+      return fail(B2DWT_EINVAL, "term out of range (src 0..3, |dm|,|dn| <= 64)");
+    }
+  }
+  p->builtin = (flags & B2DWT_FORCE_GENERIC) ? -1 : match_builtin(*p);
+  if (p->builtin >= 0) {
+    const Builtin& b = builtins()[p->builtin];
+    p->key = b.key;
+    for (const b2dwt_term& t : p->terms) p->coeffs.push_back(t.coeff);
+    p->cone = b.cone();
+  } else {
+    p->key = "generic";
+  }
+  *out = p;
+  return B2DWT_OK;
+}
+
+int b2dwt_plan_destroy(b2dwt_plan plan) {
+  delete plan;
+  return B2DWT_OK;
+}
+
+int b2dwt_plan_get_info(b2dwt_plan plan, b2dwt_plan_info* info) {
+  if (int rc = check_plan(plan)) return rc;
+  if (!info) return fail(B2DWT_EINVAL, "null info");
+  std::memset(info, 0, sizeof(*info));
+  info->kernel = plan->builtin >= 0 ? 1 : 0;
+  info->program_id = plan->builtin;
+  info->halo_left = plan->cone.left;
+  info->halo_right = plan->cone.right;
+  info->halo_up = plan->cone.up;
+  info->halo_down = plan->cone.down;
+  info->dtype = plan->dtype;
+  info->flags = plan->flags;
+  std::snprintf(info->key, sizeof(info->key), "%s", plan->key.c_str());
+  return B2DWT_OK;
+}
+
+int b2dwt_run_components(b2dwt_plan plan, const b2dwt_planes* in, const b2dwt_planes* out, int64_t rows,
+                         int64_t cols, int32_t batch, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (int rc = check_planes(in, "input")) return rc;
+  if (int rc = check_planes(out, "output")) return rc;
+  if (rows < 1 || cols < 1 || batch < 1) return fail(B2DWT_EINVAL, "empty component grid");
+  if (int rc = check_dims(2 * rows, 2 * cols)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (fused_layout_ok(*plan, 1, 1)) {
+    FusedLaunch r{};
+    r.lin = 1;
+    r.lout = 1;
+    for (int c = 0; c < 4; ++c) {
+      r.in_pl[c] = in->ptr[c];
+      r.out_pl[c] = out->ptr[c];
+    }
+    for (int c = 0; c < 4; ++c) {
+      r.in_ld[c] = in->ld[c];
+      r.out_ld[c] = out->ld[c];
+    }
+    r.in_bstride = in->bstride;
+    r.in_rows = static_cast<int>(rows);
+    r.out_bstride = out->bstride;
+    r.rows = static_cast<int>(rows);
+    r.cols = static_cast<int>(cols);
+    r.row_begin = 0;
+    r.row_end = static_cast<int>(rows);
+    r.batch = batch;
+    r.stream = s;
+    return run_fused(*plan, r);
+  }
+  const size_t es = esize(plan->dtype);
+  return run_generic(*plan, planar_views(in, es), in->bstride, planar_views(out, es), out->bstride, rows, cols,
+                     batch, s);
+}
+
+int b2dwt_forward(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t image_bstride, int64_t height,
+                  int64_t width, const b2dwt_planes* out, int32_t batch, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (int rc = check_dims(height, width)) return rc;
+  if (!image) return fail(B2DWT_EINVAL, "null image");
+  if (int rc = check_planes(out, "output")) return rc;
+  if (batch < 1) return fail(B2DWT_EINVAL, "batch must be >= 1");
+  if (image_ld < width) return fail(B2DWT_EINVAL, "image_ld < width");
+  const int64_t rows = height / 2, cols = width / 2;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (fused_layout_ok(*plan, 0, 1)) {
+    FusedLaunch r{};
+    r.lin = 0;
+    r.lout = 1;
+    r.in_img = image;
+    r.in_ld[0] = image_ld;
+    r.in_bstride = image_bstride;
+    r.in_rows = static_cast<int>(rows);
+    for (int c = 0; c < 4; ++c) {
+      r.out_pl[c] = out->ptr[c];
+      r.out_ld[c] = out->ld[c];
+    }
+    r.out_bstride = out->bstride;
+    r.rows = static_cast<int>(rows);
+    r.cols = static_cast<int>(cols);
+    r.row_begin = 0;
+    r.row_end = static_cast<int>(rows);
+    r.batch = batch;
+    r.stream = s;
+    return run_fused(*plan, r);
+  }
+  const size_t es = esize(plan->dtype);
+  return run_generic(*plan, image_views(image, image_ld, es), image_bstride, planar_views(out, es), out->bstride,
+                     rows, cols, batch, s);
+}
+
+int b2dwt_inverse(b2dwt_plan plan, const b2dwt_planes* in, void* image, int64_t image_ld, int64_t image_bstride,
+                  int64_t height, int64_t width, int32_t batch, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (int rc = check_dims(height, width)) return rc;
+  if (!image) return fail(B2DWT_EINVAL, "null image");
+  if (int rc = check_planes(in, "input")) return rc;
+  if (batch < 1) return fail(B2DWT_EINVAL, "batch must be >= 1");
+  if (image_ld < width) return fail(B2DWT_EINVAL, "image_ld < width");
+  const int64_t rows = height / 2, cols = width / 2;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (fused_layout_ok(*plan, 1, 0)) {
+    FusedLaunch r{};
+    r.lin = 1;
+    r.lout = 0;
+    for (int c = 0; c < 4; ++c) {
+      r.in_pl[c] = in->ptr[c];
+      r.in_ld[c] = in->ld[c];
+    }
+    r.in_bstride = in->bstride;
+    r.in_rows = static_cast<int>(rows);
+    r.out_img = image;
+    r.out_ld[0] = image_ld;
+    r.out_bstride = image_bstride;
+    r.rows = static_cast<int>(rows);
+    r.cols = static_cast<int>(cols);
+    r.row_begin = 0;
+    r.row_end = static_cast<int>(rows);
+    r.batch = batch;
+    r.stream = s;
+    return run_fused(*plan, r);
+  }
+  const size_t es = esize(plan->dtype);
+  return run_generic(*plan, planar_views(in, es), in->bstride, image_views(image, image_ld, es), image_bstride,
+                     rows, cols, batch, s);
+}
+
+int b2dwt_forward_rows(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t image_row0,
+                       int64_t image_rows, int64_t global_height, int64_t width, int64_t out_row_begin,
+                       int64_t out_row_end, const b2dwt_planes* out, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (int rc = check_dims(global_height, width)) return rc;
+  if (!image) return fail(B2DWT_EINVAL, "null image");
+  if (int rc = check_planes(out, "output")) return rc;
+  if (image_row0 % 2 || image_rows % 2 || image_row0 < 0 || image_rows < 2 ||
+      image_row0 + image_rows > global_height)
+    return fail(B2DWT_EINVAL, "image band must be an even-aligned row range inside the image");
+  const int64_t rows = global_height / 2, cols = width / 2;
+  if (out_row_begin < 0 || out_row_end > rows || out_row_begin >= out_row_end)
+    return fail(B2DWT_EINVAL, "bad output row range");
+  if (!fused_layout_ok(*plan, 0, 1))
+    return fail(B2DWT_EUNSUPPORTED, "row-band transform needs a fused built-in forward program");
+  const int64_t in_r0 = image_row0 / 2, in_r1 = in_r0 + image_rows / 2;
+  const int64_t need0 = std::max<int64_t>(0, out_row_begin - plan->cone.up);
+  const int64_t need1 = std::min<int64_t>(rows, out_row_end + plan->cone.down);
+  if (need0 < in_r0 || need1 > in_r1) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "band holds quad rows [%lld,%lld) but rows [%lld,%lld) are needed",
+                  static_cast<long long>(in_r0), static_cast<long long>(in_r1), static_cast<long long>(need0),
+                  static_cast<long long>(need1));
+    return fail(B2DWT_EINVAL, buf);
+  }
+  FusedLaunch r{};
+  r.lin = 0;
+  r.lout = 1;
+  r.in_img = image;
+  r.in_ld[0] = image_ld;
+  r.in_bstride = image_ld * image_rows;
+  r.in_row0 = static_cast<int>(in_r0);
+  r.in_rows = static_cast<int>(in_r1 - in_r0);
+  for (int c = 0; c < 4; ++c) {
+    r.out_pl[c] = out->ptr[c];
+    r.out_ld[c] = out->ld[c];
+  }
+  r.out_bstride = out->bstride;
+  r.out_row0 = static_cast<int>(out_row_begin);
+  r.rows = static_cast<int>(rows);
+  r.cols = static_cast<int>(cols);
+  r.row_begin = static_cast<int>(out_row_begin);
+  r.row_end = static_cast<int>(out_row_end);
+  r.batch = 1;
+  r.stream = static_cast<cudaStream_t>(stream);
+  return run_fused(*plan, r);
+}
+
+int b2dwt_dwt(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t height, int64_t width, int32_t levels,
+              const b2dwt_planes* details, void* ll_out, int64_t ll_ld, void* scratch, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (levels < 1) return fail(B2DWT_EINVAL, "levels must be >= 1");
+  if (!details || !ll_out || !image) return fail(B2DWT_EINVAL, "null pointer");
+  if ((height % (2LL << (levels - 1))) || (width % (2LL << (levels - 1))))
+    return fail(B2DWT_EINVAL, "height and width must be divisible by 2^levels");
+  if (levels > 1 && !scratch) return fail(B2DWT_EINVAL, "scratch required for levels > 1");
+  const size_t es = esize(plan->dtype);
+  char* sc[2] = {static_cast<char*>(scratch), nullptr};
+  if (scratch) sc[1] = sc[0] + static_cast<size_t>((height / 2) * (width / 2)) * es;
+  const void* in = image;
+  int64_t in_ld = image_ld;
+  for (int l = 0; l < levels; ++l) {
+    const int64_t h = height >> l, w = width >> l;
+    const b2dwt_planes& o = details[l];
+    b2dwt_planes lv = o;
+    lv.bstride = 0;
+    if (l == levels - 1) {
+      lv.ptr[0] = ll_out;
+      lv.ld[0] = ll_ld;
+    } else {
+      lv.ptr[0] = sc[l & 1];
+      lv.ld[0] = w / 2;
+    }
+    if (int rc = b2dwt_forward(plan, in, in_ld, 0, h, w, &lv, 1, stream)) return rc;
+    in = lv.ptr[0];
+    in_ld = lv.ld[0];
+  }
+  return B2DWT_OK;
+}
+
+int b2dwt_idwt(b2dwt_plan plan, const void* ll, int64_t ll_ld, const b2dwt_planes* details, int32_t levels,
+               void* image, int64_t image_ld, int64_t height, int64_t width, void* scratch, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (levels < 1) return fail(B2DWT_EINVAL, "levels must be >= 1");
+  if (!details || !ll || !image) return fail(B2DWT_EINVAL, "null pointer");
+  if ((height % (2LL << (levels - 1))) || (width % (2LL << (levels - 1))))
+    return fail(B2DWT_EINVAL, "height and width must be divisible by 2^levels");
+  if (levels > 1 && !scratch) return fail(B2DWT_EINVAL, "scratch required for levels > 1");
+  const size_t es = esize(plan->dtype);
+  char* sc[2] = {static_cast<char*>(scratch), nullptr};
+  if (scratch) sc[1] = sc[0] + static_cast<size_t>((height / 2) * (width / 2)) * es;
+  const void* cur = ll;
+  int64_t cur_ld = ll_ld;
+  for (int l = levels - 1; l >= 0; --l) {
+    const int64_t h = height >> l, w = width >> l;
+    void* dst;
+    int64_t dst_ld;
+    if (l == 0) {
+      dst = image;
+      dst_ld = image_ld;
+    } else {
+      // level l rebuilds an (H>>l) x (W>>l) LL: level 1 needs the big buffer
+      dst = sc[(l + 1) & 1];
+      dst_ld = w;
+    }
+    b2dwt_planes in = details[l];
+    in.ptr[0] = const_cast<void*>(cur);
+    in.ld[0] = cur_ld;
+    in.bstride = 0;
+    if (int rc = b2dwt_inverse(plan, &in, dst, dst_ld, 0, h, w, 1, stream)) return rc;
+    cur = dst;
+    cur_ld = dst_ld;
+  }
+  return B2DWT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,44 @@
+// launch.h -- internal host-side launch interface between the C ABI
+// (b2dwt_host.cu) and the per-program fused-kernel translation units
+// (prog_instance.cu, compiled once per built-in program structure).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace b2dwt {
+
+struct FusedLaunch {
+  int dtype;           // 0 f32, 1 f64
+  int lin, lout;       // kLayoutInterleaved / kLayoutPlanar
+  bool strict;
+  bool allow_tma;
+  // input buffer: global quad row in_row0 is buffer row 0; in_rows rows held
+  const void* in_img;
+  const void* in_pl[4];
+  int64_t in_ld[4];  // interleaved input uses in_ld[0]
+  int64_t in_bstride;
+  int in_row0, in_rows;
+  // output buffer: global quad row out_row0 is buffer row 0
+  void* out_pl[4];
+  void* out_img;
+  int64_t out_ld[4];  // interleaved output uses out_ld[0]
+  int64_t out_bstride;
+  int out_row0;
+  // global quad grid and the rows to produce
+  int rows, cols, row_begin, row_end, batch;
+  const double* coeffs;
+  int n_coeffs;
+  cudaStream_t stream;
+};
+
+// Cone of a built-in program (quads): halo the caller must provide.
+struct ConeInfo {
+  int up, down, left, right;
+};
+
+// Returns cudaSuccess or the launch error; `used_tma` reports the fill path.
+using FusedLauncher = cudaError_t (*)(const FusedLaunch&, bool* used_tma);
+using ConeGetter = ConeInfo (*)();
+
+}  // namespace b2dwt

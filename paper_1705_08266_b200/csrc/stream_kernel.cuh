@@ -1,0 +1,789 @@
+// stream_kernel.cuh -- fused single-pass 2-D DWT kernel for sm_100a.
+//
+// Replaces the reference's pass loop (liftfuse/engine.py:404-439 run_tiled ->
+// :376 _run_pass_on_tile -> :288 _apply_substep) with ONE kernel per level that
+// reads every pixel once from HBM and writes every subband sample once.
+//
+// Work decomposition
+//   A warp owns a column STRIP of 32*Q quads (Q quads per lane, adjacent) and a
+//   SEGMENT of quad rows, and walks down the rows one "tick" per quad row.
+//   Every sub-step of the program is a stage of a software pipeline held in
+//   registers:
+//     - vertical neighbours (dn != 0) live in a per-stage window of the
+//       stage's INPUT rows n-up .. n+down; row r sits in slot r mod NW, and
+//       the tick loop is unrolled by a period P (a multiple of every NW), so
+//       every slot index is a compile-time constant: no register moves;
+//     - horizontal neighbours (dm != 0) come from the adjacent lane with one
+//       __shfl per needed value ("ext" rows with left/right halo slots).
+//   Each stage reads only its own input window, so the gather semantics of the
+//   reference (every target reads the sub-step's input snapshot,
+//   engine.py:349-362) hold by construction.
+//   The dependency cone of the whole program (sum of reaches) is recomputed
+//   redundantly at strip / segment borders -- the paper's overlapping blocks
+//   (PAPER.md:287).  Only the valid interior is stored.
+//
+// Boundary semantics (engine.py:55-92, 312-347): reflection is applied to the
+// state entering EVERY sub-step.  A segment runs a few CHECKED ticks at its
+// start and end (row-range tests, top/bottom window remap through extend())
+// around an unchecked steady loop.  Strips that touch the left/right image
+// edge run a steady loop instantiated with the halo-slot reflection map; all
+// other strips run one with none of it.
+//
+// Loads are staged through a per-warp shared-memory ring (TMA tiles when the
+// row pitch allows it, per-lane cp.async otherwise); stores go straight from
+// registers as coalesced 8/16-byte vectors.
+#pragma once
+
+#include <cuda.h>
+
+#include <utility>
+
+#include "common.cuh"
+
+namespace b2dwt {
+
+constexpr int kLaneCount = 32;
+
+enum : int { kLayoutInterleaved = 0, kLayoutPlanar = 1 };
+
+template <class T, int NT>
+struct StreamArgs {
+  // input (buffer row 0 == global quad row in_row0)
+  const T* in_img;     // interleaved image (LIN == kLayoutInterleaved)
+  const T* in_pl[4];   // component planes (LIN == kLayoutPlanar)
+  int64_t in_ld[4];    // elements per image row ([0]) / per plane row
+  int64_t in_bstride;  // elements per batch item
+  int in_row0;
+  // output (buffer row 0 == global quad row out_row0)
+  T* out_pl[4];
+  T* out_img;
+  int64_t out_ld[4];
+  int64_t out_bstride;
+  int out_row0;
+  // global quad grid + work decomposition
+  int rows, cols;
+  int row_begin, row_end;  // quad rows to produce
+  int strip_w;             // valid quads per strip
+  int halo_l;              // strip's first quad = strip * strip_w - halo_l
+  int n_strips, n_segs, seg_rows, batch;
+  T k[NT];  // coefficients, flat compiled order
+};
+
+__host__ __device__ constexpr int cmod(int x, int m) { return ((x % m) + m) % m; }
+__host__ __device__ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+
+// Compile-time geometry of a program.
+template <class P>
+struct Geo {
+  static constexpr int nw(int s) { return P::reach(s).up + P::reach(s).down + 1; }
+  // input row of stage s at tick t is t - lag_in(s)
+  static constexpr int lag_in(int s) {
+    int x = 0;
+    for (int k = 0; k < s; ++k) x += P::reach(k).down;
+    return x;
+  }
+  static constexpr int sum(int which) {
+    int s = 0;
+    for (int i = 0; i < P::kNumSub; ++i) {
+      const Reach r = P::reach(i);
+      s += which == 0 ? r.up : which == 1 ? r.down : which == 2 ? r.left : r.right;
+    }
+    return s;
+  }
+  static constexpr int max_up() {
+    int m = 0;
+    for (int i = 0; i < P::kNumSub; ++i) m = P::reach(i).up > m ? P::reach(i).up : m;
+    return m;
+  }
+  static constexpr int period() {
+    int p = 1;
+    for (int i = 0; i < P::kNumSub; ++i) p = p / cgcd(p, nw(i)) * nw(i);
+    return p;
+  }
+  static constexpr int up = sum(0), down = sum(1), left = sum(2), right = sum(3);
+  static constexpr int kPeriod = period();
+  static constexpr int kMaxUp = max_up();
+};
+
+// Kept for the host: cone of a program.
+template <class P>
+using Cone = Geo<P>;
+
+// ---------------------------------------------------------------------------
+// Per-warp runtime context shared by all pipeline stages.
+struct Ctx {
+  int rows, cols;
+  int first;     // first quad row any stage computes (segment start - cone)
+  int n0, n1;    // rows stored
+  int m_lane;    // global quad column of this lane's slot 0
+  int m_strip;   // global quad column of lane 0's slot 0
+};
+
+template <class T>
+__device__ __forceinline__ T shfl_idx(T v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+template <class T>
+__device__ __forceinline__ T shfl_up1(T v) {
+  return __shfl_up_sync(0xffffffffu, v, 1);
+}
+template <class T>
+__device__ __forceinline__ T shfl_down1(T v) {
+  return __shfl_down_sync(0xffffffffu, v, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Pipeline stage S (sub-step S of program P).
+template <class P, class T, int Q, bool kStrict, int S, bool kEnd = (S == P::kNumSub)>
+struct Stage;
+
+template <class P, class T, int Q, bool kStrict, int S>
+struct Stage<P, T, Q, kStrict, S, false> {
+  static constexpr Reach kR = P::reach(S);
+  static constexpr int U = kR.up, D = kR.down, L = kR.left, R = kR.right;
+  static constexpr int NW = U + D + 1;
+  static constexpr int E = L + Q + R;
+  static constexpr int kLag = Geo<P>::lag_in(S);
+  static_assert(L <= Q && R <= Q, "horizontal reach must not exceed the lane width");
+  static_assert(Geo<P>::kPeriod % NW == 0, "period must be a multiple of every window");
+  using Ar = Arith<kStrict>;
+  using Next = Stage<P, T, Q, kStrict, S + 1>;
+
+  T w[NW][4][E];  // input row r (with halo) lives in slot r mod NW
+  Next next;
+
+  // One tick: append input row (t - kLag), compute row n = t - kLag - D.
+  template <int PH, bool CHECK, bool HEDGE, class Args, class Sink>
+  __device__ __forceinline__ void tick(const T (&in)[4][Q], int t, const Ctx& cx, const Args& a, Sink& sink) {
+    constexpr int kSlotIn = cmod(PH - kLag, NW);
+    append<HEDGE>(in, w[kSlotIn], cx);
+    constexpr int kOff = cmod(PH - kLag - D, NW);  // slot of row n
+    T out[4][Q];
+    if constexpr (!CHECK) {
+      eval<kOff>(w, out, a);
+      next.template tick<PH, false, HEDGE>(out, t, cx, a, sink);
+    } else {
+      // Rows past the bottom edge are not computed, but the tick is still
+      // forwarded so later stages with lookahead can finish their last rows
+      // (they reflect instead of reading the placeholder).
+      const int n = t - kLag - D;
+      if (n >= cx.first) {
+        if (n < cx.rows) {
+          if ((U > 0 || D > 0) && (n - U < 0 || n + D >= cx.rows)) {
+            T vw[NW][4][E];
+            remap_rows(n, cx, vw);
+            eval<U>(vw, out, a);  // logical order: slot(dn) = U + dn
+          } else {
+            eval<kOff>(w, out, a);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int q = 0; q < Q; ++q) out[c][q] = T(0);
+        }
+        next.template tick<PH, true, HEDGE>(out, t, cx, a, sink);
+      }
+    }
+  }
+
+  // Window row = input row plus left/right halo from the neighbour lanes.
+  template <bool HEDGE>
+  __device__ __forceinline__ static void append(const T (&in)[4][Q], T (&x)[4][E], const Ctx& cx) {
+    append_comp<0, HEDGE>(in, x[0], cx);
+    append_comp<1, HEDGE>(in, x[1], cx);
+    append_comp<2, HEDGE>(in, x[2], cx);
+    append_comp<3, HEDGE>(in, x[3], cx);
+  }
+
+  template <int C, bool HEDGE>
+  __device__ __forceinline__ static void append_comp(const T (&in)[4][Q], T (&x)[E], const Ctx& cx) {
+    constexpr CompNeed nd = P::need(S, C);
+    if constexpr (nd.used) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) x[L + q] = in[C][q];
+      if constexpr (!HEDGE) {
+#pragma unroll
+        for (int e = 0; e < L; ++e)
+          if (L - e <= nd.left) x[e] = shfl_up1(in[C][Q - L + e]);
+#pragma unroll
+        for (int e = 0; e < R; ++e)
+          if (e < nd.right) x[L + Q + e] = shfl_down1(in[C][e]);
+      } else {
+        // Image-edge strip: every slot a neighbour read can reach goes through
+        // the reflection map -- own slots too, since the image edge may fall
+        // inside a lane (odd component widths).
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const bool needed = (nd.left > 0 || nd.right > 0) && e >= L - nd.left && e < L + Q + nd.right;
+          if (!needed) continue;
+          const int col = reflect(cx.m_lane - L + e, col_parity(C), cx.cols);
+          const int rel = col - cx.m_strip;
+          int src = rel / Q;
+          const int slot = rel - src * Q;
+          src = src < 0 ? 0 : (src > kLaneCount - 1 ? kLaneCount - 1 : src);
+          T v = shfl_idx(in[C][0], src);
+#pragma unroll
+          for (int j = 1; j < Q; ++j) {
+            const T tt = shfl_idx(in[C][j], src);
+            v = (slot == j) ? tt : v;
+          }
+          x[e] = v;
+        }
+      }
+    }
+  }
+
+  // Top / bottom rows: rebuild the window in logical order through the row
+  // reflection map (reflected rows are always inside the window).
+  __device__ __forceinline__ void remap_rows(int n, const Ctx& cx, T (&vw)[NW][4][E]) const {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int rp = row_parity(c);
+#pragma unroll
+      for (int p = 0; p < NW; ++p) {
+        const int src = reflect(n - U + p, rp, cx.rows) % NW;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          T v = w[0][c][e];
+#pragma unroll
+          for (int j = 1; j < NW; ++j) v = (src == j) ? w[j][c][e] : v;
+          vw[p][c][e] = v;
+        }
+      }
+    }
+  }
+
+  template <int OFF, int TGT, int K, class Args>
+  __device__ __forceinline__ static void term(const T (&win)[NW][4][E], T (&acc)[Q], const Args& a) {
+    constexpr int idx = P::begin(S * 4 + TGT) + K;
+    constexpr TermInfo ti = P::term(idx);
+    constexpr int slot = cmod(OFF + ti.dn, NW);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const T x = win[slot][ti.src][L + q + ti.dm];
+      if constexpr (K == 0) {
+        acc[q] = ti.unit ? x : Ar::mul(x, a.k[idx]);
+      } else {
+        acc[q] = ti.unit ? Ar::add(acc[q], x) : Ar::mac(acc[q], x, a.k[idx]);
+      }
+    }
+  }
+
+  template <int OFF, int TGT, class Args, int... K>
+  __device__ __forceinline__ static void target(const T (&win)[NW][4][E], T (&acc)[Q], const Args& a,
+                                                std::integer_sequence<int, K...>) {
+    (term<OFF, TGT, K>(win, acc, a), ...);
+  }
+
+  template <int OFF, int TGT, class Args>
+  __device__ __forceinline__ static void eval_target(const T (&win)[NW][4][E], T (&out)[4][Q], const Args& a) {
+    constexpr int cnt = P::begin(S * 4 + TGT + 1) - P::begin(S * 4 + TGT);
+    if constexpr (cnt == 0) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) out[TGT][q] = T(0);
+    } else {
+      target<OFF, TGT>(win, out[TGT], a, std::make_integer_sequence<int, cnt>{});
+    }
+  }
+
+  template <int OFF, class Args>
+  __device__ __forceinline__ static void eval(const T (&win)[NW][4][E], T (&out)[4][Q], const Args& a) {
+    eval_target<OFF, 0>(win, out, a);
+    eval_target<OFF, 1>(win, out, a);
+    eval_target<OFF, 2>(win, out, a);
+    eval_target<OFF, 3>(win, out, a);
+  }
+};
+
+// End of the pipeline: hand the finished row (t - sum of lookaheads) to the sink.
+template <class P, class T, int Q, bool kStrict, int S>
+struct Stage<P, T, Q, kStrict, S, true> {
+  template <int PH, bool CHECK, bool HEDGE, class Args, class Sink>
+  __device__ __forceinline__ void tick(const T (&in)[4][Q], int t, const Ctx& cx, const Args& a, Sink& sink) {
+    const int n = t - Geo<P>::down;
+    if constexpr (CHECK) {
+      if (n < cx.n0 || n >= cx.n1) return;
+    }
+    sink.store(in, n);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Output sinks: per-lane base pointers precomputed once per warp.
+template <class T, int Q, int LOUT>
+struct StoreSink;
+
+// Four planes, Q consecutive quads per lane.
+template <class T, int Q>
+struct StoreSink<T, Q, kLayoutPlanar> {
+  T* base[4];      // plane c at row 0 of the global grid, this lane's column
+  int64_t ld[4];
+  bool full, vec;  // all Q slots stored / vector store legal
+  unsigned mask;   // per-slot store mask when !full
+
+  template <class Args>
+  __device__ __forceinline__ void init(const Args& a, int64_t boff, int m_lane, int vlo, int vhi) {
+    bool v = true;
+    mask = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (m_lane + q >= vlo && m_lane + q < vhi) mask |= 1u << q;
+    full = mask == (1u << Q) - 1;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      ld[c] = a.out_ld[c];
+      base[c] = a.out_pl[c] + boff - static_cast<int64_t>(a.out_row0) * ld[c] + m_lane;
+      v = v && (ld[c] % Q == 0) && (reinterpret_cast<uintptr_t>(base[c]) % (sizeof(T) * Q) == 0);
+    }
+    vec = v;
+  }
+
+  __device__ __forceinline__ void store(const T (&v)[4][Q], int n) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      T* p = base[c] + static_cast<int64_t>(n) * ld[c];
+      if (full && vec) {
+        if constexpr (Q == 2 && sizeof(T) == 4) {
+          *reinterpret_cast<float2*>(p) = make_float2(v[c][0], v[c][1]);
+        } else if constexpr (Q == 2 && sizeof(T) == 8) {
+          *reinterpret_cast<double2*>(p) = make_double2(v[c][0], v[c][1]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < Q; ++q) p[q] = v[c][q];
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (mask & (1u << q)) p[q] = v[c][q];
+      }
+    }
+  }
+};
+
+// Interleaved image: quad (n, m) -> pixels (2n, 2m) .. (2n+1, 2m+1).
+template <class T, int Q>
+struct StoreSink<T, Q, kLayoutInterleaved> {
+  T* base;
+  int64_t ld;
+  bool full, vec;
+  unsigned mask;
+
+  template <class Args>
+  __device__ __forceinline__ void init(const Args& a, int64_t boff, int m_lane, int vlo, int vhi) {
+    mask = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (m_lane + q >= vlo && m_lane + q < vhi) mask |= 1u << q;
+    full = mask == (1u << Q) - 1;
+    ld = a.out_ld[0];
+    base = a.out_img + boff - 2 * static_cast<int64_t>(a.out_row0) * ld + 2 * m_lane;
+    vec = (ld * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0;
+  }
+
+  __device__ __forceinline__ void store(const T (&v)[4][Q], int n) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      T* p = base + static_cast<int64_t>(2 * n + h) * ld;
+      T px[2 * Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        px[2 * q] = v[2 * h][q];
+        px[2 * q + 1] = v[2 * h + 1][q];
+      }
+      if (full && vec) {
+#pragma unroll
+        for (int i = 0; i < 2 * Q; i += 16 / static_cast<int>(sizeof(T))) {
+          if constexpr (sizeof(T) == 4) {
+            *reinterpret_cast<float4*>(p + i) = make_float4(px[i], px[i + 1], px[i + 2], px[i + 3]);
+          } else {
+            *reinterpret_cast<double2*>(p + i) = make_double2(px[i], px[i + 1]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (mask & (1u << q)) {
+            p[2 * q] = px[2 * q];
+            p[2 * q + 1] = px[2 * q + 1];
+          }
+      }
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// cp.async / TMA primitives.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Copy BYTES (multiple of 4, <= 32) with the widest cp.async the alignment allows.
+template <int BYTES>
+__device__ __forceinline__ void cp_chunk(char* s, const char* g) {
+  const uintptr_t al = reinterpret_cast<uintptr_t>(g);
+  if constexpr (BYTES % 16 == 0) {
+    if ((al & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < BYTES; i += 16) cp_async16(s + i, g + i);
+      return;
+    }
+  }
+  if constexpr (BYTES % 8 == 0) {
+    if ((al & 7) == 0) {
+#pragma unroll
+      for (int i = 0; i < BYTES; i += 8) cp_async8(s + i, g + i);
+      return;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < BYTES; i += 4) cp_async4(s + i, g + i);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];\n" ::"r"(s),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(b), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Per-warp shared-memory ring.  One stage = RPS quad rows of 4*Q*32 elements,
+// laid out exactly like the TMA box that fills it:
+//   interleaved input: [2*RPS image rows][64*Q pixels]
+//   planar input:      [4 planes][RPS rows][32*Q quads]
+// so the cp.async fill path writes the same layout and one reader serves both.
+template <class T, int Q>
+struct RowGeom {
+  static constexpr int kElems = 4 * Q * kLaneCount;
+  static constexpr int kBytes = kElems * static_cast<int>(sizeof(T));
+};
+
+template <int Q, int LIN, int RPS>
+__device__ __forceinline__ constexpr int stage_offset(int j, int hc) {
+  return LIN == kLayoutInterleaved ? (2 * j + hc) * (2 * Q * kLaneCount) : (hc * RPS + j) * (Q * kLaneCount);
+}
+
+template <class T, int Q, int LIN, int RPS>
+__device__ __forceinline__ void read_row(const T* stage, int j, int lane, T (&r)[4][Q]) {
+  if constexpr (LIN == kLayoutInterleaved) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const T* p = stage + stage_offset<Q, LIN, RPS>(j, h) + 2 * Q * lane;
+      T px[2 * Q];
+#pragma unroll
+      for (int i = 0; i < 2 * Q; i += 16 / static_cast<int>(sizeof(T))) {
+        if constexpr (sizeof(T) == 4) {
+          const float4 f = *reinterpret_cast<const float4*>(p + i);
+          px[i] = f.x;
+          px[i + 1] = f.y;
+          px[i + 2] = f.z;
+          px[i + 3] = f.w;
+        } else {
+          const double2 f = *reinterpret_cast<const double2*>(p + i);
+          px[i] = f.x;
+          px[i + 1] = f.y;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        r[2 * h][q] = px[2 * q];
+        r[2 * h + 1][q] = px[2 * q + 1];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const T* p = stage + stage_offset<Q, LIN, RPS>(j, c) + Q * lane;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) r[c][q] = p[q];
+    }
+  }
+}
+
+template <class T, int Q, int LIN, int RPS, class Args>
+__device__ __forceinline__ void fill_row_cpasync(T* stage, int j, int gr, int64_t boff, int lane, int m_lane,
+                                                 int cols, const Args& a) {
+  const int64_t br = gr - a.in_row0;  // buffer quad row
+  const bool full = m_lane >= 0 && m_lane + Q <= cols;
+  if constexpr (LIN == kLayoutInterleaved) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const T* g = a.in_img + boff + (2 * br + h) * a.in_ld[0] + 2 * m_lane;
+      T* s = stage + stage_offset<Q, LIN, RPS>(j, h) + 2 * Q * lane;
+      if (full) {
+        cp_chunk<2 * Q * sizeof(T)>(reinterpret_cast<char*>(s), reinterpret_cast<const char*>(g));
+      } else {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int m = m_lane + q;
+          if (m >= 0 && m < cols)
+            cp_chunk<2 * sizeof(T)>(reinterpret_cast<char*>(s + 2 * q), reinterpret_cast<const char*>(g + 2 * q));
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const T* g = a.in_pl[c] + boff + br * a.in_ld[c] + m_lane;
+      T* s = stage + stage_offset<Q, LIN, RPS>(j, c) + Q * lane;
+      if (full) {
+        cp_chunk<Q * sizeof(T)>(reinterpret_cast<char*>(s), reinterpret_cast<const char*>(g));
+      } else {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int m = m_lane + q;
+          if (m >= 0 && m < cols)
+            cp_chunk<sizeof(T)>(reinterpret_cast<char*>(s + q), reinterpret_cast<const char*>(g + q));
+        }
+      }
+    }
+  }
+}
+
+// Streams quad rows first .. last_load of one (strip, segment) through the ring.
+template <class T, int Q, int LIN, bool kTma, int STAGES, int RPS>
+struct RowSource {
+  static constexpr int kStageElems = RPS * RowGeom<T, Q>::kElems;
+  T* ring;
+  uint64_t* bars;
+  int first, last_load, n_stages;
+  int k, j;  // current stage, row within it
+  const T* slot;
+  int lane, m_lane, m_strip, cols, b;
+  int64_t boff;
+
+  template <class Args>
+  __device__ __forceinline__ void issue(int kk, const Args& a, const CUtensorMap* tm0, const CUtensorMap* tm1,
+                                        const CUtensorMap* tm2, const CUtensorMap* tm3) {
+    T* s = ring + (kk % STAGES) * kStageElems;
+    if constexpr (kTma) {
+      if (lane == 0) {
+        uint64_t* bar = bars + (kk % STAGES);
+        mbar_expect_tx(bar, kStageElems * sizeof(T));
+        const int r0 = first + kk * RPS - a.in_row0;
+        if constexpr (LIN == kLayoutInterleaved) {
+          tma_load_3d(s, tm0, bar, 2 * m_strip, 2 * r0, b);
+        } else {
+          constexpr int kPlane = RPS * Q * kLaneCount;
+          tma_load_3d(s + 0 * kPlane, tm0, bar, m_strip, r0, b);
+          tma_load_3d(s + 1 * kPlane, tm1, bar, m_strip, r0, b);
+          tma_load_3d(s + 2 * kPlane, tm2, bar, m_strip, r0, b);
+          tma_load_3d(s + 3 * kPlane, tm3, bar, m_strip, r0, b);
+        }
+      }
+    } else {
+      if (kk < n_stages) {
+#pragma unroll 1
+        for (int jj = 0; jj < RPS; ++jj) {
+          const int gr = first + kk * RPS + jj;
+          if (gr <= last_load) fill_row_cpasync<T, Q, LIN, RPS>(s, jj, gr, boff, lane, m_lane, cols, a);
+        }
+      }
+      cp_async_commit();
+    }
+  }
+
+  template <class Args>
+  __device__ __forceinline__ void start(const Args& a, const CUtensorMap* tm0, const CUtensorMap* tm1,
+                                        const CUtensorMap* tm2, const CUtensorMap* tm3) {
+    n_stages = (last_load - first + RPS) / RPS;
+    if constexpr (kTma) {
+      if (lane == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(bars + s, 1);
+        fence_mbar_init();
+      }
+      __syncwarp();
+      for (int kk = 0; kk < STAGES - 1 && kk < n_stages; ++kk) issue(kk, a, tm0, tm1, tm2, tm3);
+    } else {
+      for (int kk = 0; kk < STAGES - 1; ++kk) issue(kk, a, tm0, tm1, tm2, tm3);
+    }
+    k = -1;
+    j = RPS - 1;
+  }
+
+  // Next quad row (rows are consumed strictly in order).
+  template <class Args>
+  __device__ __forceinline__ void next(T (&row)[4][Q], const Args& a, const CUtensorMap* tm0,
+                                       const CUtensorMap* tm1, const CUtensorMap* tm2, const CUtensorMap* tm3) {
+    if (++j == RPS) {
+      j = 0;
+      ++k;
+      if constexpr (kTma) {
+        mbar_wait(bars + (k % STAGES), (k / STAGES) & 1);
+        __syncwarp();
+        // slot (k-1) % STAGES was consumed in the previous round: refill it
+        if (k + STAGES - 1 < n_stages) {
+          if (lane == 0) fence_proxy_async();
+          issue(k + STAGES - 1, a, tm0, tm1, tm2, tm3);
+        }
+      } else {
+        cp_async_wait<STAGES - 2>();
+        issue(k + STAGES - 1, a, tm0, tm1, tm2, tm3);
+      }
+      slot = ring + (k % STAGES) * kStageElems;
+    }
+    read_row<T, Q, LIN, RPS>(slot, j, lane, row);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Tick helpers (everything force-inlined: the pipeline must stay in registers).
+template <int PH, bool CHECK, bool HEDGE, class Pipe, class T, int Q, class Args, class Sink>
+__device__ __forceinline__ void run_tick(Pipe& pipe, const T (&row)[4][Q], int t, const Ctx& cx, const Args& a,
+                                         Sink& sink) {
+  pipe.template tick<PH, CHECK, HEDGE>(row, t, cx, a, sink);
+}
+
+// Checked tick at runtime phase t % P.
+template <int P, bool HEDGE, class Pipe, class T, int Q, class Args, class Sink, int... I>
+__device__ __forceinline__ void checked_tick(Pipe& pipe, const T (&row)[4][Q], int t, const Ctx& cx, const Args& a,
+                                             Sink& sink, std::integer_sequence<int, I...>) {
+  const int ph = t % P;
+  ((ph == I ? run_tick<I, true, HEDGE>(pipe, row, t, cx, a, sink) : void()), ...);
+}
+
+// P unchecked ticks t .. t+P-1 (t % P == 0).
+template <bool HEDGE, class T, int Q, class Pipe, class Src, class Args, class Sink, int... I>
+__device__ __forceinline__ void steady_chunk(Pipe& pipe, Src& src, int t, const Ctx& cx, const Args& a, Sink& sink,
+                                             const CUtensorMap* m0, const CUtensorMap* m1, const CUtensorMap* m2,
+                                             const CUtensorMap* m3, std::integer_sequence<int, I...>) {
+  T row[sizeof...(I)][4][Q];
+  // One row at a time: load, then push through every stage.
+  ((src.next(row[I], a, m0, m1, m2, m3), run_tick<I, false, HEDGE>(pipe, row[I], t + I, cx, a, sink)), ...);
+}
+
+// ---------------------------------------------------------------------------
+// The kernel.
+//   P        program structure (programs.inc)
+//   T        float | double
+//   Q        quads per lane
+//   LIN/LOUT input / output layout
+//   kTma     fill the ring with TMA (requires 16 B pitches) instead of cp.async
+template <class P, class T, int Q, int LIN, int LOUT, bool kStrict, bool kTma, int WARPS, int STAGES, int RPS>
+__global__ void __launch_bounds__(WARPS* kLaneCount)
+    stream_kernel(const __grid_constant__ StreamArgs<T, (P::kNumTerms > 0 ? P::kNumTerms : 1)> a,
+                  const __grid_constant__ CUtensorMap tmap0, const __grid_constant__ CUtensorMap tmap1,
+                  const __grid_constant__ CUtensorMap tmap2, const __grid_constant__ CUtensorMap tmap3) {
+  using G = Geo<P>;
+  using Src = RowSource<T, Q, LIN, kTma, STAGES, RPS>;
+  using Sink = StoreSink<T, Q, LOUT>;
+  using Pipe = Stage<P, T, Q, kStrict, 0>;
+  constexpr int kP = G::kPeriod;
+  using Phases = std::make_integer_sequence<int, kP>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+
+  const int warp = threadIdx.x / kLaneCount;
+  const int lane = threadIdx.x % kLaneCount;
+  const int unit = blockIdx.x * WARPS + warp;
+  const int total = a.batch * a.n_segs * a.n_strips;
+  if (unit >= total) return;  // warp-uniform; no block-wide barrier follows
+  const int strip = unit % a.n_strips;
+  const int seg = (unit / a.n_strips) % a.n_segs;
+  const int b = unit / (a.n_strips * a.n_segs);
+
+  Ctx cx;
+  cx.rows = a.rows;
+  cx.cols = a.cols;
+  cx.m_strip = strip * a.strip_w - a.halo_l;
+  cx.m_lane = cx.m_strip + Q * lane;
+  const bool hedge = cx.m_strip < 0 || cx.m_strip + Q * kLaneCount > a.cols;
+  cx.n0 = a.row_begin + seg * a.seg_rows;
+  cx.n1 = min(cx.n0 + a.seg_rows, a.row_end);
+  cx.first = max(0, cx.n0 - G::up);
+  const int last_load = min(a.rows - 1, cx.n1 - 1 + G::down);
+  const int last_tick = cx.n1 - 1 + G::down;
+
+  Src src;
+  src.ring = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(warp) * STAGES * Src::kStageElems;
+  src.bars = reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(WARPS) * STAGES * Src::kStageElems * sizeof(T)) +
+             warp * STAGES;
+  src.first = cx.first;
+  src.last_load = last_load;
+  src.lane = lane;
+  src.m_lane = cx.m_lane;
+  src.m_strip = cx.m_strip;
+  src.cols = a.cols;
+  src.b = b;
+  src.boff = static_cast<int64_t>(b) * a.in_bstride;
+  src.start(a, &tmap0, &tmap1, &tmap2, &tmap3);
+
+  Sink sink;
+  sink.init(a, static_cast<int64_t>(b) * a.out_bstride, cx.m_lane, max(strip * a.strip_w, 0),
+            min(strip * a.strip_w + a.strip_w, a.cols));
+
+  // Window rows above the segment's first loaded row only ever feed rows that
+  // are not stored; start them at zero so nothing uninitialised is read.
+  Pipe pipe{};
+
+  // Steady range: every stage interior, every row loaded and stored.
+  const int steady_lo = G::down + max(cx.n0, G::kMaxUp);
+  const int steady_hi = min(a.rows - 1, cx.n1 - 1 + G::down);
+#pragma unroll 1
+  for (int t = cx.first; t <= last_tick;) {
+    if (t >= steady_lo && t % kP == 0 && t + kP - 1 <= steady_hi) {
+      if (hedge)
+        steady_chunk<true, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, Phases{});
+      else
+        steady_chunk<false, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, Phases{});
+      t += kP;
+    } else {
+      T row[4][Q];
+      if (t <= last_load) {
+        src.next(row, a, &tmap0, &tmap1, &tmap2, &tmap3);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int q = 0; q < Q; ++q) row[c][q] = T(0);
+      }
+      if (hedge)
+        checked_tick<kP, true>(pipe, row, t, cx, a, sink, Phases{});
+      else
+        checked_tick<kP, false>(pipe, row, t, cx, a, sink, Phases{});
+      ++t;
+    }
+  }
+  if constexpr (!kTma) cp_async_wait<0>();
+}
+
+}  // namespace b2dwt

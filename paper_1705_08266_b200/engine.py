@@ -1,0 +1,533 @@
+"""Public transform API -- a drop-in for ``liftfuse.engine`` backed by sm_100a kernels.
+
+Same names, argument meaning and error behaviour as the reference
+(``liftfuse/engine.py``):
+
+==========================  =====================================================
+reference                   here
+==========================  =====================================================
+``forward`` :481-487        :func:`forward` -- one fused kernel (deinterleave +
+                            all passes + subband stores), ``b2dwt_forward``
+``inverse`` :490-495        :func:`inverse` -- fused ``b2dwt_inverse``
+``run_tiled`` :404-439      :func:`run_tiled` -- ``b2dwt_run_components``;
+                            ``TileConfig`` is validated like the reference
+                            (tile >= halo) and then ignored: GPU tiling is
+                            internal and results do not depend on it
+``run_reference`` :442-451  :func:`run_reference` (same device path)
+``Image2D`` / ``SubbandQuad`` / ``TileConfig`` / ``deinterleave`` /
+``interleave_quad`` / ``extend`` / ``compile_scheme`` -- same data types
+==========================  =====================================================
+
+New (north star): :func:`dwt` / :func:`idwt` multi-level pyramids, and the
+device-tensor API :class:`Transform` that the benchmarks and multi-GPU paths
+use (inputs stay resident in HBM; no host round trip).
+
+Schemes may be this package's (:func:`.lifting.build_scheme`) or the
+reference's own ``liftfuse.schemes.Scheme`` objects (duck-typed).
+Arithmetic is "strict" by default: bit-identical to the reference.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .lifting import EXACT, Laurent, LiftingPlan, Scheme, build_scheme, invert_scheme
+from .program import StencilProgram, compile_scheme, extend
+
+__all__ = [
+    "PRECISION_DTYPES",
+    "Image2D",
+    "SubbandQuad",
+    "Pyramid",
+    "TileConfig",
+    "StencilProgram",
+    "Transform",
+    "extend",
+    "compile_scheme",
+    "forward",
+    "inverse",
+    "dwt",
+    "idwt",
+    "run_tiled",
+    "run_reference",
+    "deinterleave",
+    "interleave_quad",
+]
+
+PRECISION_DTYPES = {"single": np.float32, "double": np.float64}
+
+
+# -- data types (engine.py:95-197) ----------------------------------------------------
+
+
+@dataclass(frozen=True)
+class Image2D:
+    """Row-major real-valued raster (engine.py:95-144)."""
+
+    data: np.ndarray
+
+    def __post_init__(self):
+        arr = np.asarray(self.data)
+        if arr.ndim != 2 or arr.shape[0] < 1 or arr.shape[1] < 1:
+            raise ValueError("image data must be a non-empty 2-D array")
+        if arr.dtype not in (np.float32, np.float64):
+            arr = arr.astype(np.float64)
+        object.__setattr__(self, "data", arr)
+
+    @property
+    def width(self) -> int:
+        return self.data.shape[1]
+
+    @property
+    def height(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def precision(self) -> str:
+        return "single" if self.data.dtype == np.float32 else "double"
+
+    @classmethod
+    def random(cls, width: int, height: int, seed: int, precision: str = "double") -> "Image2D":
+        rng = np.random.default_rng(seed)
+        return cls(rng.random((height, width), dtype=np.float64).astype(PRECISION_DTYPES[precision]))
+
+    @classmethod
+    def constant(cls, width: int, height: int, value: float = 1.0, precision: str = "double") -> "Image2D":
+        return cls(np.full((height, width), value, dtype=PRECISION_DTYPES[precision]))
+
+    @classmethod
+    def delta(cls, width: int, height: int, row: int, col: int, precision: str = "double") -> "Image2D":
+        data = np.zeros((height, width), dtype=PRECISION_DTYPES[precision])
+        data[row, col] = 1.0
+        return cls(data)
+
+    def astype(self, precision: str) -> "Image2D":
+        return Image2D(self.data.astype(PRECISION_DTYPES[precision]))
+
+
+@dataclass(frozen=True)
+class SubbandQuad:
+    """The four polyphase subbands of one level (engine.py:147-176)."""
+
+    ll: Image2D
+    hl: Image2D
+    lh: Image2D
+    hh: Image2D
+
+    def __post_init__(self):
+        shape = self.ll.data.shape
+        for band in (self.hl, self.lh, self.hh):
+            if band.data.shape != shape:
+                raise ValueError("all four subbands must share dimensions")
+
+    def components(self) -> list:
+        return [self.ll.data, self.hl.data, self.lh.data, self.hh.data]
+
+    def interleave(self) -> Image2D:
+        return Image2D(interleave_quad(self.components()))
+
+    @classmethod
+    def from_components(cls, comps) -> "SubbandQuad":
+        ll, hl, lh, hh = (Image2D(c) for c in comps)
+        return cls(ll, hl, lh, hh)
+
+
+@dataclass(frozen=True)
+class Pyramid:
+    """Multi-level result: ``details[l] = (hl, lh, hh)`` of level l (finest
+    first) and the coarsest ``ll``.  Level l transforms level l-1's LL."""
+
+    ll: Image2D
+    details: tuple
+
+    @property
+    def levels(self) -> int:
+        return len(self.details)
+
+
+@dataclass(frozen=True)
+class TileConfig:
+    """Accepted and validated like the reference (engine.py:179-197); the GPU
+    decomposition is internal and the result is independent of it."""
+
+    tile: tuple | None = None
+    threads: int = 1
+
+    def __post_init__(self):
+        if self.tile is not None:
+            tw, th = self.tile
+            if tw < 1 or th < 1:
+                raise ValueError("tile dimensions must be positive")
+        if self.threads < 1:
+            raise ValueError("thread count must be positive")
+
+
+def deinterleave(image: Image2D) -> list:
+    """Host-side polyphase split (engine.py:200-211); the GPU path fuses it."""
+    a = image.data
+    if a.shape[0] % 2 or a.shape[1] % 2:
+        raise ValueError(f"dimensions must be even, got {a.shape[1]}x{a.shape[0]}")
+    return [np.ascontiguousarray(a[r::2, c::2]) for r, c in ((0, 0), (0, 1), (1, 0), (1, 1))]
+
+
+def interleave_quad(comps) -> np.ndarray:
+    """Host-side polyphase merge (engine.py:214-221); the GPU path fuses it."""
+    rows, cols = comps[0].shape
+    out = np.empty((2 * rows, 2 * cols), dtype=comps[0].dtype)
+    out[0::2, 0::2], out[0::2, 1::2], out[1::2, 0::2], out[1::2, 1::2] = comps
+    return out
+
+
+# -- scheme adoption ----------------------------------------------------------------
+
+
+def _adopt_plan(plan) -> LiftingPlan:
+    if isinstance(plan, LiftingPlan):
+        return plan
+    mode = getattr(plan, "mode", EXACT)
+    pairs = tuple((Laurent(dict(p.terms), mode), Laurent(dict(u.terms), mode)) for p, u in plan.pairs)
+    return LiftingPlan(plan.name, pairs, plan.scale, mode)
+
+
+def _adopt_scheme(scheme) -> Scheme:
+    """This package's Scheme for a (possibly foreign, duck-typed) scheme."""
+    if isinstance(scheme, Scheme):
+        return scheme
+    s = build_scheme(scheme.name, _adopt_plan(scheme.plan))
+    return invert_scheme(s) if getattr(scheme, "inverted", False) else s
+
+
+def _programs(scheme):
+    """(forward program, inverse program) of a scheme."""
+    fwd = compile_scheme(scheme)
+    inv = compile_scheme(invert_scheme(_adopt_scheme(scheme)))
+    return fwd, inv
+
+
+def _check_tile(cfg: TileConfig, program) -> None:
+    if cfg.tile is not None:
+        tw, th = cfg.tile
+        halo = program.halo
+        if tw < halo or th < halo:
+            raise ValueError(f"tile {tw}x{th} is smaller than the scheme halo {halo}")
+
+
+# -- device plumbing ------------------------------------------------------------------
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _require_cuda():
+    torch = _torch()
+    _native.load()
+    if not torch.cuda.is_available():
+        raise _native.NativeError("no CUDA device visible: the b2dwt kernels need a B200 (no CPU fallback)")
+    return torch
+
+
+_NP2NATIVE = {np.dtype(np.float32): _native.F32, np.dtype(np.float64): _native.F64}
+
+
+def _signature(program):
+    return tuple(tuple(sub.terms) for p in program.passes for sub in p.substeps)
+
+
+_PLAN_CACHE: dict = {}
+
+
+def plan_for(program, dtype: int, flags: int = 0) -> _native.Plan:
+    """Cached native plan for a compiled program."""
+    key = (_signature(program), dtype, flags)
+    plan = _PLAN_CACHE.get(key)
+    if plan is None:
+        plan = _native.Plan(program, dtype, flags)
+        _PLAN_CACHE[key] = plan
+    return plan
+
+
+def _stream_handle(torch, stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes_void(s.cuda_stream)
+
+
+def ctypes_void(x):
+    import ctypes
+
+    return ctypes.c_void_p(int(x))
+
+
+def _ptr(t) -> int:
+    return int(t.data_ptr())
+
+
+class Transform:
+    """Device-resident transform for one scheme at one precision.
+
+    All tensors are CUDA tensors; calls are asynchronous on the current torch
+    stream (or ``stream``).  ``x`` is ``[H, W]`` or ``[B, H, W]`` (contiguous
+    rows; any row pitch via ``stride``).
+    """
+
+    def __init__(self, scheme, precision: str = "single", fast: bool = False, tma: bool = True,
+                 force_generic: bool = False):
+        self.scheme = scheme
+        self.precision = precision
+        self.np_dtype = np.dtype(PRECISION_DTYPES[precision])
+        self.dtype = _NP2NATIVE[self.np_dtype]
+        flags = _native.FAST if fast else 0
+        if not tma:
+            flags |= _native.NO_TMA
+        if force_generic:
+            flags |= _native.FORCE_GENERIC
+        self.flags = flags
+        self.fwd_program, self.inv_program = _programs(scheme)
+        self.fwd_plan = plan_for(self.fwd_program, self.dtype, flags)
+        self.inv_plan = plan_for(self.inv_program, self.dtype, flags)
+
+    @property
+    def torch_dtype(self):
+        torch = _torch()
+        return torch.float32 if self.dtype == _native.F32 else torch.float64
+
+    def _check(self, t, name):
+        torch = _require_cuda()
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise TypeError(f"{name} must be a CUDA tensor")
+        if t.dtype != self.torch_dtype:
+            raise TypeError(f"{name} must be {self.torch_dtype}, got {t.dtype}")
+        if t.stride(-1) != 1:
+            raise ValueError(f"{name} rows must be contiguous")
+        return torch
+
+    # single level --------------------------------------------------------------------
+    def forward(self, x, out=None, stream=None):
+        """Return (ll, hl, lh, hh), each ``[..., H/2, W/2]``."""
+        torch = self._check(x, "x")
+        batched = x.dim() == 3
+        xb = x if batched else x.unsqueeze(0)
+        b, h, w = xb.shape
+        if h % 2 or w % 2:
+            raise ValueError(f"dimensions must be even, got {w}x{h}")
+        if out is None:
+            out = tuple(torch.empty((b, h // 2, w // 2), dtype=x.dtype, device=x.device) for _ in range(4))
+        else:
+            out = tuple(o if o.dim() == 3 else o.unsqueeze(0) for o in out)
+        pl = _native.planes([_ptr(o) for o in out], [o.stride(1) for o in out], out[0].stride(0))
+        _native.check(
+            _native.load().b2dwt_forward(self.fwd_plan.handle, _ptr(xb), xb.stride(1), xb.stride(0), h, w, pl, b,
+                                         _stream_handle(torch, stream)),
+            "forward",
+        )
+        return out if batched else tuple(o[0] for o in out)
+
+    def inverse(self, ll, hl, lh, hh, out=None, stream=None):
+        torch = self._check(ll, "ll")
+        comps = [c if c.dim() == 3 else c.unsqueeze(0) for c in (ll, hl, lh, hh)]
+        shape = comps[0].shape
+        for c in comps[1:]:
+            if c.shape != shape:
+                raise ValueError("all four subbands must share dimensions")
+        b, rows, cols = shape
+        if out is None:
+            out = torch.empty((b, 2 * rows, 2 * cols), dtype=ll.dtype, device=ll.device)
+        ob = out if out.dim() == 3 else out.unsqueeze(0)
+        pl = _native.planes([_ptr(c) for c in comps], [c.stride(1) for c in comps], comps[0].stride(0))
+        _native.check(
+            _native.load().b2dwt_inverse(self.inv_plan.handle, pl, _ptr(ob), ob.stride(1), ob.stride(0), 2 * rows,
+                                         2 * cols, b, _stream_handle(torch, stream)),
+            "inverse",
+        )
+        return ob if ll.dim() == 3 else ob[0]
+
+    def run_components(self, comps, program=None, out=None, stream=None):
+        torch = self._check(comps[0], "comps")
+        plan = self.fwd_plan if program is None else plan_for(program, self.dtype, self.flags)
+        cs = [c if c.dim() == 3 else c.unsqueeze(0) for c in comps]
+        b, rows, cols = cs[0].shape
+        if out is None:
+            out = [torch.empty_like(c) for c in cs]
+        pin = _native.planes([_ptr(c) for c in cs], [c.stride(1) for c in cs], cs[0].stride(0))
+        pout = _native.planes([_ptr(c) for c in out], [c.stride(1) for c in out], out[0].stride(0))
+        _native.check(
+            _native.load().b2dwt_run_components(plan.handle, pin, pout, rows, cols, b,
+                                                _stream_handle(torch, stream)),
+            "run_components",
+        )
+        return out if comps[0].dim() == 3 else [o[0] for o in out]
+
+    def forward_rows(self, band, band_row0, global_height, out_row_begin, out_row_end, out=None, stream=None):
+        """Forward transform of quad rows [out_row_begin, out_row_end) of a
+        global_height x W image from a row band that starts at pixel row
+        ``band_row0`` (must include the cone; see :attr:`cone`)."""
+        torch = self._check(band, "band")
+        rows_b, w = band.shape
+        n = out_row_end - out_row_begin
+        if out is None:
+            out = tuple(torch.empty((n, w // 2), dtype=band.dtype, device=band.device) for _ in range(4))
+        pl = _native.planes([_ptr(o) for o in out], [o.stride(0) for o in out], 0)
+        _native.check(
+            _native.load().b2dwt_forward_rows(self.fwd_plan.handle, _ptr(band), band.stride(0), band_row0, rows_b,
+                                              global_height, w, out_row_begin, out_row_end, pl,
+                                              _stream_handle(torch, stream)),
+            "forward_rows",
+        )
+        return out
+
+    @property
+    def cone(self):
+        """(up, down, left, right) dependency cone of the fused forward kernel, quads."""
+        return self.fwd_plan.cone
+
+    # multi level -----------------------------------------------------------------------
+    def dwt(self, x, levels: int, stream=None):
+        """Return (ll, [(hl, lh, hh) per level, finest first])."""
+        torch = self._check(x, "x")
+        if x.dim() != 2:
+            raise ValueError("dwt takes one [H, W] image")
+        h, w = x.shape
+        if levels < 1:
+            raise ValueError("levels must be >= 1")
+        if h % (1 << levels) or w % (1 << levels):
+            raise ValueError(f"dimensions must be divisible by 2^{levels}, got {w}x{h}")
+        details = []
+        for lvl in range(levels):
+            hh_, ww_ = h >> (lvl + 1), w >> (lvl + 1)
+            details.append(tuple(torch.empty((hh_, ww_), dtype=x.dtype, device=x.device) for _ in range(3)))
+        ll = torch.empty((h >> levels, w >> levels), dtype=x.dtype, device=x.device)
+        scratch = torch.empty(((h // 2) * (w // 2) + (h // 4) * (w // 4),), dtype=x.dtype, device=x.device) \
+            if levels > 1 else None
+        self.dwt_into(x, levels, details, ll, scratch, stream)
+        return ll, details
+
+    def dwt_into(self, x, levels, details, ll, scratch, stream=None):
+        torch = _torch()
+        arr = (_native.Planes * levels)()
+        for lvl, (hl, lh, hh) in enumerate(details):
+            arr[lvl] = _native.planes([0, _ptr(hl), _ptr(lh), _ptr(hh)],
+                                      [0, hl.stride(0), lh.stride(0), hh.stride(0)], 0)
+        h, w = x.shape
+        _native.check(
+            _native.load().b2dwt_dwt(self.fwd_plan.handle, _ptr(x), x.stride(0), h, w, levels, arr, _ptr(ll),
+                                     ll.stride(0), _ptr(scratch) if scratch is not None else None,
+                                     _stream_handle(torch, stream)),
+            "dwt",
+        )
+
+    def idwt(self, ll, details, out=None, stream=None):
+        torch = self._check(ll, "ll")
+        levels = len(details)
+        h, w = ll.shape[0] << levels, ll.shape[1] << levels
+        if out is None:
+            out = torch.empty((h, w), dtype=ll.dtype, device=ll.device)
+        scratch = torch.empty(((h // 2) * (w // 2) + (h // 4) * (w // 4),), dtype=ll.dtype, device=ll.device) \
+            if levels > 1 else None
+        arr = (_native.Planes * levels)()
+        for lvl, (hl, lh, hh) in enumerate(details):
+            arr[lvl] = _native.planes([0, _ptr(hl), _ptr(lh), _ptr(hh)],
+                                      [0, hl.stride(0), lh.stride(0), hh.stride(0)], 0)
+        _native.check(
+            _native.load().b2dwt_idwt(self.inv_plan.handle, _ptr(ll), ll.stride(0), arr, levels, _ptr(out),
+                                      out.stride(0), h, w, _ptr(scratch) if scratch is not None else None,
+                                      _stream_handle(torch, stream)),
+            "idwt",
+        )
+        return out
+
+
+_TRANSFORMS: dict = {}
+
+
+def _transform(scheme, precision: str) -> Transform:
+    key = (id(scheme), precision)
+    t = _TRANSFORMS.get(key)
+    if t is None or t.scheme is not scheme:
+        t = Transform(scheme, precision)
+        _TRANSFORMS[key] = t
+    return t
+
+
+def _to_device(torch, arr: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(arr)).to("cuda", non_blocking=False)
+
+
+def _to_host(t) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+# -- reference-shaped host API ------------------------------------------------------------
+
+
+def forward(image: Image2D, scheme, cfg: TileConfig | None = None) -> SubbandQuad:
+    """Single-level forward transform of an even-dimensioned image (engine.py:481-487)."""
+    cfg = cfg or TileConfig()
+    program = compile_scheme(scheme)
+    a = image.data
+    if a.shape[0] % 2 or a.shape[1] % 2:
+        raise ValueError(f"dimensions must be even, got {a.shape[1]}x{a.shape[0]}")
+    _check_tile(cfg, program)
+    torch = _require_cuda()
+    tr = _transform(scheme, image.precision)
+    comps = tr.forward(_to_device(torch, a))
+    return SubbandQuad.from_components([_to_host(c) for c in comps])
+
+
+def inverse(quad: SubbandQuad, scheme, cfg: TileConfig | None = None) -> Image2D:
+    """Invert :func:`forward`; ``scheme`` is the forward scheme (engine.py:490-495)."""
+    cfg = cfg or TileConfig()
+    program = compile_scheme(invert_scheme(_adopt_scheme(scheme)))
+    _check_tile(cfg, program)
+    torch = _require_cuda()
+    tr = _transform(scheme, quad.ll.precision)
+    comps = [_to_device(torch, c) for c in quad.components()]
+    return Image2D(_to_host(tr.inverse(*comps)))
+
+
+def run_tiled(program, comps, cfg: TileConfig) -> list:
+    """Run a compiled program over 4 component arrays (engine.py:404-439)."""
+    if cfg.tile is not None:
+        _check_tile(cfg, program)
+    torch = _require_cuda()
+    dtype = np.dtype(comps[0].dtype)
+    if dtype not in _NP2NATIVE:
+        raise TypeError("components must be float32 or float64")
+    plan = plan_for(program, _NP2NATIVE[dtype])
+    dev = [_to_device(torch, c) for c in comps]
+    out = [torch.empty_like(d) for d in dev]
+    rows, cols = comps[0].shape
+    pin = _native.planes([_ptr(c) for c in dev], [c.stride(0) for c in dev], 0)
+    pout = _native.planes([_ptr(c) for c in out], [c.stride(0) for c in out], 0)
+    _native.check(
+        _native.load().b2dwt_run_components(plan.handle, pin, pout, rows, cols, 1, _stream_handle(torch, None)),
+        "run_tiled",
+    )
+    return [_to_host(o) for o in out]
+
+
+def run_reference(program, comps) -> list:
+    """Untiled executor (engine.py:442-451): the same device path."""
+    return run_tiled(program, comps, TileConfig())
+
+
+def dwt(image: Image2D, scheme, levels: int = 1, cfg: TileConfig | None = None) -> Pyramid:
+    """Multi-level forward transform: level l is :func:`forward` of level l-1's LL."""
+    cfg = cfg or TileConfig()
+    _check_tile(cfg, compile_scheme(scheme))
+    torch = _require_cuda()
+    tr = _transform(scheme, image.precision)
+    ll, details = tr.dwt(_to_device(torch, image.data), levels)
+    return Pyramid(Image2D(_to_host(ll)), tuple(tuple(Image2D(_to_host(b)) for b in d) for d in details))
+
+
+def idwt(pyramid: Pyramid, scheme, cfg: TileConfig | None = None) -> Image2D:
+    """Invert :func:`dwt` level by level, coarsest first."""
+    torch = _require_cuda()
+    tr = _transform(scheme, pyramid.ll.precision)
+    details = [tuple(_to_device(torch, b.data) for b in d) for d in pyramid.details]
+    return Image2D(_to_host(tr.idwt(_to_device(torch, pyramid.ll.data), details)))

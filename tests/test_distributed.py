@@ -1,0 +1,108 @@
+"""CPU (gloo, world_size 2 and 4): the multi-GPU partitioning logic.
+
+The row-strip path exchanges the fused kernel's cone with its neighbours and
+transforms bands through ``band_forward``.  Here ``band_forward`` is an
+oracle-backed stand-in for ``Transform.forward_rows`` (tests only), so the
+exchange, band and halo bookkeeping is verified bit-for-bit against the
+single-process oracle on CPU.  The GPU kernel behind ``forward_rows`` is
+checked against whole-image transforms in tests/test_gpu_parity.py.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle
+from paper_1705_08266_b200 import CDF53, CDF97, build_scheme, compile_scheme
+from paper_1705_08266_b200.distributed import RowStrips, shard_range
+
+CONES = {"cdf97": (2, 2), "cdf53": (1, 1)}
+PLANS = {"cdf97": CDF97, "cdf53": CDF53}
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _oracle_band_forward(prog):
+    def band_forward(band, band_row0, height, r0, r1, out):
+        # forward_rows semantics: the band's own edges are reflected by the
+        # oracle, which is harmless because [r0, r1) lies a full cone inside
+        # any band edge that is not a global edge.
+        q = oracle.forward(band.numpy(), prog, threads=1)
+        bq0 = band_row0 // 2
+        for o, c in zip(out, q):
+            o.copy_(torch.from_numpy(c[r0 - bq0:r1 - bq0]))
+    return band_forward
+
+
+def _worker(rank, world, port, wavelet, levels, overlap, h, w, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        prog = compile_scheme(build_scheme("non-separable-split", PLANS[wavelet]))
+        img = np.random.default_rng(7).random((h, w)).astype(np.float32)
+        strips = RowStrips(h, w, rank, world, CONES[wavelet], levels=levels)
+        buf = strips.allocate(lambda s: torch.zeros(s, dtype=torch.float32))
+        L = strips.layout(0)
+        strips.owned(buf).copy_(torch.from_numpy(img[L.row0:L.row0 + L.rows]))
+        ll, details = strips.dwt(_oracle_band_forward(prog), buf, lambda s: torch.zeros(s, dtype=torch.float32),
+                                 overlap=overlap)
+        want_ll, want_det = oracle.dwt(img, prog, levels)
+        ok = True
+        for lvl, (got, want) in enumerate(zip(details, want_det)):
+            Ll = strips.layout(lvl)
+            a, b = Ll.row0 // 2, (Ll.row0 + Ll.rows) // 2
+            for g, wv in zip(got, want):
+                ok &= np.array_equal(g.numpy(), wv[a:b])
+        Ll = strips.layout(levels - 1)
+        a, b = Ll.row0 // 2, (Ll.row0 + Ll.rows) // 2
+        ok &= np.array_equal(ll.numpy(), want_ll[a:b])
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,wavelet,levels,overlap,h,w", [
+    (2, "cdf97", 1, True, 64, 40),
+    (2, "cdf97", 3, False, 128, 48),
+    (4, "cdf53", 2, True, 96, 36),
+    (4, "cdf97", 2, True, 160, 36),
+])
+def test_row_strips_bitwise_equal_single_process(world, wavelet, levels, overlap, h, w):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, wavelet, levels, overlap, h, w, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(results[r] for r in range(world)), results
+
+
+def test_shard_range_partitions():
+    for n in (0, 1, 7, 1024):
+        for world in (1, 2, 3, 8):
+            spans = [shard_range(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+
+
+def test_row_strips_validation():
+    with pytest.raises(ValueError):
+        RowStrips(100, 64, 0, 8, (2, 2))  # 100 not divisible by 16
+    with pytest.raises(ValueError):
+        RowStrips(16, 32, 0, 8, (2, 2))  # strips thinner than the halo
+    s = RowStrips(4096, 64, 1, 4, (2, 2), levels=1)
+    L = s.layout(0)
+    assert (L.row0, L.rows, L.halo_top, L.halo_bot) == (1024, 1024, 4, 4)

@@ -1,0 +1,234 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) vs the reference.
+
+Every comparison here is against outputs the real reference produced
+(tests/golden/, bit-exact) or against the oracle that was pinned to them
+(tests/test_oracle.py).  Strict mode (the default) must be BIT-IDENTICAL;
+fast (FMA) mode must stay within the north star's 1e-4 x input range (f32).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from tests import golden_data as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1705_08266_b200 import _native  # noqa: E402
+from paper_1705_08266_b200.engine import Transform, plan_for  # noqa: E402
+
+NAMES = ("ll", "hl", "lh", "hh")
+
+
+class _GoldenScheme:
+    """Scheme stand-in that carries the reference's own compiled programs."""
+
+
+def _transform_from_programs(fwd_prog, inv_prog, precision, **kw):
+    t = Transform.__new__(Transform)
+    t.scheme = None
+    t.precision = precision
+    t.np_dtype = np.dtype(np.float32 if precision == "single" else np.float64)
+    t.dtype = _native.F32 if precision == "single" else _native.F64
+    flags = 0
+    if kw.get("fast"):
+        flags |= _native.FAST
+    if kw.get("tma") is False:
+        flags |= _native.NO_TMA
+    if kw.get("force_generic"):
+        flags |= _native.FORCE_GENERIC
+    t.flags = flags
+    t.fwd_program, t.inv_program = fwd_prog, inv_prog
+    t.fwd_plan = plan_for(fwd_prog, t.dtype, flags)
+    t.inv_plan = plan_for(inv_prog, t.dtype, flags)
+    return t
+
+
+def _golden_transform(wavelet, scheme, precision, **kw):
+    progs = G.programs()
+    return _transform_from_programs(progs[f"{wavelet}/{scheme}/fwd"], progs[f"{wavelet}/{scheme}/inv"], precision, **kw)
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _host(t):
+    return t.cpu().numpy()
+
+
+VARIANTS = [dict(), dict(tma=False), dict(force_generic=True)]
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=["fused-tma", "fused-cpasync", "generic"])
+def test_vectors_bit_exact(variant):
+    vec = G.vectors()
+    checked = 0
+    for k in G.hashes():
+        wavelet, scheme, direction, w, h, seed, precision = G.parse_key(k)
+        if f"{k}/img" not in vec and f"{k}/ll" not in vec:
+            continue
+        tr = _golden_transform(wavelet, scheme, precision, **variant)
+        if direction == "fwd":
+            img = G.random_image(w, h, seed, precision)
+            got = [_host(c) for c in tr.forward(_dev(img))]
+            for c, name in enumerate(NAMES):
+                assert np.array_equal(got[c], vec[f"{k}/{name}"]), (k, name, tr.fwd_plan.key)
+        else:
+            kf = k.replace("/inv/", "/fwd/")
+            comps = [_dev(vec[f"{kf}/{n}"]) for n in NAMES]
+            got = _host(tr.inverse(*comps))
+            assert np.array_equal(got, vec[f"{k}/img"]), (k, tr.inv_plan.key)
+        checked += 1
+    assert checked >= 500
+
+
+def test_fused_kernel_selected_for_cdf_programs():
+    for wavelet in ("cdf53", "cdf97", "asym"):
+        for scheme in ("separable-convolution", "separable-lifting", "non-separable-lifting", "non-separable-split"):
+            tr = _golden_transform(wavelet, scheme, "single")
+            assert tr.fwd_plan.fused and tr.inv_plan.fused, (wavelet, scheme)
+    assert not _golden_transform("haar-like", "non-separable-split", "single").fwd_plan.fused
+
+
+@pytest.mark.parametrize("variant", VARIANTS[:2], ids=["fused-tma", "fused-cpasync"])
+def test_hashes_bit_exact(variant):
+    checked = 0
+    for k, digest in G.hashes().items():
+        wavelet, scheme, direction, w, h, seed, precision = G.parse_key(k)
+        tr = _golden_transform(wavelet, scheme, precision, **variant)
+        img = G.random_image(w, h, seed, precision)
+        fwd = tr.forward(_dev(img))
+        if direction == "fwd":
+            assert G.sha([_host(c) for c in fwd]) == digest, k
+        else:
+            # the inverse consumes the reference's forward output: regenerate it
+            # through the (already hash-verified) forward of the same run
+            assert G.sha([_host(tr.inverse(*fwd))]) == digest, k
+        checked += 1
+    assert checked > 300
+
+
+def test_run_components_matches_oracle():
+    progs = G.programs()
+    rng = np.random.default_rng(5)
+    for key in ("cdf97/non-separable-split/fwd", "cdf53/separable-lifting/inv", "cdf97/separable-convolution/inv",
+                "haar-like/non-separable-lifting/fwd"):
+        prog = progs[key]
+        for dtype in (np.float32, np.float64):
+            comps = [rng.random((37, 53)).astype(dtype) for _ in range(4)]
+            want = oracle.run_reference(prog, comps)
+            tr = _transform_from_programs(prog, prog, "single" if dtype == np.float32 else "double")
+            got = tr.run_components([_dev(c) for c in comps], program=prog)
+            for g, w in zip(got, want):
+                assert np.array_equal(_host(g), w), key
+
+
+@pytest.mark.parametrize("shape", [(4096, 4096), (2050, 3074), (520, 8200)])
+def test_large_strict_bit_exact_vs_oracle(shape):
+    """Full-size strict parity at C2 size and ragged shapes (multi-strip, multi-segment)."""
+    progs = G.programs()
+    h, w = shape
+    img = np.random.default_rng(11).random((h, w)).astype(np.float32)
+    for scheme in ("non-separable-split", "separable-convolution"):
+        tr = _golden_transform("cdf97", scheme, "single")
+        got = [_host(c) for c in tr.forward(_dev(img))]
+        want = oracle.forward(img, progs[f"cdf97/{scheme}/fwd"])
+        for g, wv, n in zip(got, want, NAMES):
+            assert np.array_equal(g, wv), (scheme, shape, n, np.argwhere(g != wv)[:5])
+        rec = _host(tr.inverse(*[_dev(c) for c in got]))
+        want_rec = oracle.inverse(want, progs[f"cdf97/{scheme}/inv"])
+        assert np.array_equal(rec, want_rec), (scheme, shape)
+
+
+def test_fast_mode_within_north_star_tolerance():
+    progs = G.programs()
+    img = np.random.default_rng(3).random((1030, 2050)).astype(np.float32)
+    rng_ = float(img.max() - img.min())
+    for wavelet in ("cdf53", "cdf97"):
+        for scheme in ("separable-convolution", "separable-lifting", "non-separable-lifting", "non-separable-split"):
+            tr = _golden_transform(wavelet, scheme, "single", fast=True)
+            got = [_host(c) for c in tr.forward(_dev(img))]
+            want = oracle.forward(img.astype(np.float64), progs[f"{wavelet}/{scheme}/fwd"])
+            err = max(float(np.abs(g - wv).max()) for g, wv in zip(got, want))
+            assert err <= 1e-4 * rng_, (wavelet, scheme, err)
+
+
+def test_batch_equals_loop():
+    tr = _golden_transform("cdf97", "non-separable-split", "single")
+    x = torch.rand((3, 130, 262), device="cuda")
+    batched = tr.forward(x)
+    for b in range(3):
+        single = tr.forward(x[b].contiguous())
+        for cb, cs in zip(batched, single):
+            assert torch.equal(cb[b], cs)
+    rec = tr.inverse(*batched)
+    for b in range(3):
+        assert torch.equal(rec[b], tr.inverse(*[c[b].contiguous() for c in batched]))
+
+
+@pytest.mark.parametrize("wavelet", ["cdf53", "cdf97"])
+def test_forward_rows_band_equals_full(wavelet):
+    """Row-strip building block of the multi-GPU path: bitwise equal to the
+    same rows of the whole-image transform."""
+    tr = _golden_transform(wavelet, "non-separable-split", "single")
+    h, w = 512, 300
+    x = torch.rand((h, w), device="cuda")
+    full = tr.forward(x)
+    up, down = tr.cone[0], tr.cone[1]
+    rows = h // 2
+    for (r0, r1) in [(0, 64), (64, 128), (200, 256), (0, 256), (17, 93)]:
+        b0 = max(0, r0 - up)
+        b1 = min(rows, r1 + down)
+        band = x[2 * b0:2 * b1].contiguous()
+        out = tr.forward_rows(band, 2 * b0, h, r0, r1)
+        for o, f in zip(out, full):
+            assert torch.equal(o, f[r0:r1]), (r0, r1)
+
+
+def test_pyramids_match_iterated_reference():
+    pyr = G.pyramids()
+    bases = sorted({k.rsplit("/", 1)[0] if k.endswith(("/ll", "/rec")) else k.rsplit("/", 2)[0] for k in pyr})
+    for base in bases:
+        wavelet, scheme, dims, seed, lv, precision = base.split("/")
+        w, h = (int(x) for x in dims.split("x"))
+        levels = int(lv[1:])
+        img = G.random_image(w, h, int(seed[1:]), precision)
+        tr = _golden_transform(wavelet, scheme, precision)
+        ll, details = tr.dwt(_dev(img), levels)
+        assert np.array_equal(_host(ll), pyr[f"{base}/ll"]), base
+        for lvl, bands in enumerate(details):
+            for name, band in zip(("hl", "lh", "hh"), bands):
+                assert np.array_equal(_host(band), pyr[f"{base}/{lvl}/{name}"]), (base, lvl, name)
+        rec = _host(tr.idwt(ll, details))
+        assert np.array_equal(rec, pyr[f"{base}/rec"]), base
+
+
+def test_public_api_round_trip():
+    from paper_1705_08266_b200 import CDF97, SCHEME_NAMES, Image2D, build_scheme, dwt, forward, idwt, inverse
+
+    img = Image2D.random(66, 34, seed=4, precision="single")
+    for name in SCHEME_NAMES:
+        s = build_scheme(name, CDF97)
+        q = forward(img, s)
+        rec = inverse(q, s)
+        assert rec.data.dtype == np.float32
+        assert float(np.abs(rec.data - img.data).max()) <= 1e-3
+    big = Image2D.random(256, 128, seed=1, precision="double")
+    s = build_scheme("non-separable-split", CDF97)
+    p = dwt(big, s, levels=4)
+    assert p.ll.data.shape == (8, 16)
+    assert float(np.abs(idwt(p, s).data - big.data).max()) <= 1e-9
+
+
+def test_errors_match_reference_messages():
+    from paper_1705_08266_b200 import CDF53, CDF97, Image2D, TileConfig, build_scheme, forward
+
+    with pytest.raises(ValueError, match="dimensions must be even"):
+        forward(Image2D(np.zeros((5, 8))), build_scheme("separable-lifting", CDF53))
+    with pytest.raises(ValueError, match="smaller than the scheme halo"):
+        forward(Image2D.random(32, 32, seed=0), build_scheme("separable-convolution", CDF97), TileConfig(tile=(1, 1)))
