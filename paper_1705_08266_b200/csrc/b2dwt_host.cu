@@ -222,6 +222,10 @@ int run_fused(const b2dwt_plan_s& p, FusedLaunch& r) {
   r.allow_tma = (p.flags & B2DWT_NO_TMA) == 0;
   r.coeffs = p.coeffs.data();
   r.n_coeffs = static_cast<int>(p.coeffs.size());
+  // Small levels are latency-bound (a tick is a long dependent chain), so
+  // spread them over the whole machine; 8 rows keeps the cone re-read <= 50%
+  // there and negligible on large levels, which fill the machine anyway.
+  r.min_rows_per_warp = 8;
   bool used_tma = false;
   const cudaError_t e = b.launch(r, &used_tma);
   if (e != cudaSuccess) return cuda_fail(e, "fused stream kernel");

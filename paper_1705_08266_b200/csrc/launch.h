@@ -29,6 +29,7 @@ struct FusedLaunch {
   int rows, cols, row_begin, row_end, batch;
   const double* coeffs;
   int n_coeffs;
+  int min_rows_per_warp;  // work split: lower bound on rows per warp (latency vs cone overhead)
   cudaStream_t stream;
 };
 

@@ -147,15 +147,15 @@ cudaError_t launch(const FusedLaunch& r) {
   a.strip_w = strip_w;
   a.halo_l = halo_l;
   a.n_strips = (r.cols + strip_w - 1) / strip_w;
-  // segments: enough warps for ~one full wave, but never shorter than 32 rows
+  // Work split: the flat (item, strip, row) space is divided evenly over at
+  // most one full wave of resident warps (each warp >= min_rows rows so the
+  // per-segment cone overhead stays bounded).
+  const int64_t kMinRows = std::max(1, r.min_rows_per_warp);
   const int rows_out = r.row_end - r.row_begin;
   const int64_t resident = static_cast<int64_t>(num_sms()) * blocks_per_sm * kWarps;
-  const int64_t per_seg = static_cast<int64_t>(r.batch) * a.n_strips;
-  int n_segs = static_cast<int>(std::max<int64_t>(1, (resident + per_seg - 1) / per_seg));
-  n_segs = std::min(n_segs, std::max(1, rows_out / 32));
-  int seg_rows = (rows_out + n_segs - 1) / n_segs;
-  a.seg_rows = seg_rows;
-  a.n_segs = (rows_out + seg_rows - 1) / seg_rows;
+  const int64_t total_rows = static_cast<int64_t>(r.batch) * a.n_strips * rows_out;
+  const int64_t n_warps = std::max<int64_t>(1, std::min(resident, (total_rows + kMinRows - 1) / kMinRows));
+  a.n_warps = static_cast<int>(n_warps);
 
   CUtensorMap maps[4];
   memset(maps, 0, sizeof(maps));
@@ -171,8 +171,7 @@ cudaError_t launch(const FusedLaunch& r) {
           return cudaErrorNotSupported;
     }
   }
-  const int64_t units = per_seg * a.n_segs;
-  const unsigned grid = static_cast<unsigned>((units + kWarps - 1) / kWarps);
+  const unsigned grid = static_cast<unsigned>((n_warps + kWarps - 1) / kWarps);
   kern<<<grid, kWarps * kLaneCount, kSmem, r.stream>>>(a, maps[0], maps[1], maps[2], maps[3]);
   return cudaGetLastError();
 }

@@ -65,7 +65,8 @@ struct StreamArgs {
   int row_begin, row_end;  // quad rows to produce
   int strip_w;             // valid quads per strip
   int halo_l;              // strip's first quad = strip * strip_w - halo_l
-  int n_strips, n_segs, seg_rows, batch;
+  int n_strips, batch;
+  int n_warps;              // warps sharing the flat (item, strip, row) space
   T k[NT];  // coefficients, flat compiled order
 };
 
@@ -320,6 +321,7 @@ struct StoreSink<T, Q, kLayoutPlanar> {
   T* base[4];      // plane c at row 0 of the global grid, this lane's column
   int64_t ld[4];
   bool full, vec;  // all Q slots stored / vector store legal
+  bool any_scalar; // some lane of the warp stores slot by slot
   unsigned mask;   // per-slot store mask when !full
 
   template <class Args>
@@ -337,6 +339,7 @@ struct StoreSink<T, Q, kLayoutPlanar> {
       v = v && (ld[c] % Q == 0) && (reinterpret_cast<uintptr_t>(base[c]) % (sizeof(T) * Q) == 0);
     }
     vec = v;
+    any_scalar = __any_sync(0xffffffffu, mask != 0 && !(full && vec));
   }
 
   __device__ __forceinline__ void store(const T (&v)[4][Q], int n) {
@@ -352,10 +355,13 @@ struct StoreSink<T, Q, kLayoutPlanar> {
 #pragma unroll
           for (int q = 0; q < Q; ++q) p[q] = v[c][q];
         }
-      } else {
+      }
+      if (any_scalar) {  // warp-uniform: only warps that own ragged / unaligned lanes
+        if (!(full && vec)) {
 #pragma unroll
-        for (int q = 0; q < Q; ++q)
-          if (mask & (1u << q)) p[q] = v[c][q];
+          for (int q = 0; q < Q; ++q)
+            if (mask & (1u << q)) p[q] = v[c][q];
+        }
       }
     }
   }
@@ -366,7 +372,7 @@ template <class T, int Q>
 struct StoreSink<T, Q, kLayoutInterleaved> {
   T* base;
   int64_t ld;
-  bool full, vec;
+  bool full, vec, any_scalar;
   unsigned mask;
 
   template <class Args>
@@ -379,6 +385,7 @@ struct StoreSink<T, Q, kLayoutInterleaved> {
     ld = a.out_ld[0];
     base = a.out_img + boff - 2 * static_cast<int64_t>(a.out_row0) * ld + 2 * m_lane;
     vec = (ld * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0;
+    any_scalar = __any_sync(0xffffffffu, mask != 0 && !(full && vec));
   }
 
   __device__ __forceinline__ void store(const T (&v)[4][Q], int n) {
@@ -400,13 +407,16 @@ struct StoreSink<T, Q, kLayoutInterleaved> {
             *reinterpret_cast<double2*>(p + i) = make_double2(px[i], px[i + 1]);
           }
         }
-      } else {
+      }
+      if (any_scalar) {
+        if (!(full && vec)) {
 #pragma unroll
-        for (int q = 0; q < Q; ++q)
-          if (mask & (1u << q)) {
-            p[2 * q] = px[2 * q];
-            p[2 * q + 1] = px[2 * q + 1];
-          }
+          for (int q = 0; q < Q; ++q)
+            if (mask & (1u << q)) {
+              p[2 * q] = px[2 * q];
+              p[2 * q + 1] = px[2 * q + 1];
+            }
+        }
       }
     }
   }
@@ -587,7 +597,8 @@ struct RowSource {
   T* ring;
   uint64_t* bars;
   int first, last_load, n_stages;
-  int k, j;  // current stage, row within it
+  int k, j;   // current stage within the segment, row within the stage
+  int base;   // stages consumed by earlier segments (mbarrier phase continuity)
   const T* slot;
   int lane, m_lane, m_strip, cols, b;
   int64_t boff;
@@ -595,10 +606,11 @@ struct RowSource {
   template <class Args>
   __device__ __forceinline__ void issue(int kk, const Args& a, const CUtensorMap* tm0, const CUtensorMap* tm1,
                                         const CUtensorMap* tm2, const CUtensorMap* tm3) {
-    T* s = ring + (kk % STAGES) * kStageElems;
+    const int g = base + kk;
+    T* s = ring + (g % STAGES) * kStageElems;
     if constexpr (kTma) {
       if (lane == 0) {
-        uint64_t* bar = bars + (kk % STAGES);
+        uint64_t* bar = bars + (g % STAGES);
         mbar_expect_tx(bar, kStageElems * sizeof(T));
         const int r0 = first + kk * RPS - a.in_row0;
         if constexpr (LIN == kLayoutInterleaved) {
@@ -623,22 +635,37 @@ struct RowSource {
     }
   }
 
-  template <class Args>
-  __device__ __forceinline__ void start(const Args& a, const CUtensorMap* tm0, const CUtensorMap* tm1,
-                                        const CUtensorMap* tm2, const CUtensorMap* tm3) {
-    n_stages = (last_load - first + RPS) / RPS;
+  __device__ __forceinline__ void init_barriers() {
+    base = 0;
     if constexpr (kTma) {
       if (lane == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(bars + s, 1);
         fence_mbar_init();
       }
       __syncwarp();
+    }
+  }
+
+  // Begin a segment: rows first .. last_load will be consumed in order.
+  template <class Args>
+  __device__ __forceinline__ void start(const Args& a, const CUtensorMap* tm0, const CUtensorMap* tm1,
+                                        const CUtensorMap* tm2, const CUtensorMap* tm3) {
+    n_stages = (last_load - first + RPS) / RPS;
+    if constexpr (kTma) {
+      __syncwarp();  // every lane is done reading the previous segment's slots
+      if (lane == 0) fence_proxy_async();
       for (int kk = 0; kk < STAGES - 1 && kk < n_stages; ++kk) issue(kk, a, tm0, tm1, tm2, tm3);
     } else {
       for (int kk = 0; kk < STAGES - 1; ++kk) issue(kk, a, tm0, tm1, tm2, tm3);
     }
     k = -1;
     j = RPS - 1;
+  }
+
+  // End a segment (all its stages were consumed).
+  __device__ __forceinline__ void finish() {
+    base += n_stages;
+    if constexpr (!kTma) cp_async_wait<0>();
   }
 
   // Next quad row (rows are consumed strictly in order).
@@ -648,10 +675,11 @@ struct RowSource {
     if (++j == RPS) {
       j = 0;
       ++k;
+      const int g = base + k;
       if constexpr (kTma) {
-        mbar_wait(bars + (k % STAGES), (k / STAGES) & 1);
+        mbar_wait(bars + (g % STAGES), (g / STAGES) & 1);
         __syncwarp();
-        // slot (k-1) % STAGES was consumed in the previous round: refill it
+        // slot (g-1) % STAGES was consumed in the previous round: refill it
         if (k + STAGES - 1 < n_stages) {
           if (lane == 0) fence_proxy_async();
           issue(k + STAGES - 1, a, tm0, tm1, tm2, tm3);
@@ -660,7 +688,7 @@ struct RowSource {
         cp_async_wait<STAGES - 2>();
         issue(k + STAGES - 1, a, tm0, tm1, tm2, tm3);
       }
-      slot = ring + (k % STAGES) * kStageElems;
+      slot = ring + (g % STAGES) * kStageElems;
     }
     read_row<T, Q, LIN, RPS>(slot, j, lane, row);
   }
@@ -714,76 +742,92 @@ __global__ void __launch_bounds__(WARPS* kLaneCount)
 
   const int warp = threadIdx.x / kLaneCount;
   const int lane = threadIdx.x % kLaneCount;
-  const int unit = blockIdx.x * WARPS + warp;
-  const int total = a.batch * a.n_segs * a.n_strips;
-  if (unit >= total) return;  // warp-uniform; no block-wide barrier follows
-  const int strip = unit % a.n_strips;
-  const int seg = (unit / a.n_strips) % a.n_segs;
-  const int b = unit / (a.n_strips * a.n_segs);
+  const int gw = blockIdx.x * WARPS + warp;
+  if (gw >= a.n_warps) return;  // warp-uniform; no block-wide barrier follows
 
-  Ctx cx;
-  cx.rows = a.rows;
-  cx.cols = a.cols;
-  cx.m_strip = strip * a.strip_w - a.halo_l;
-  cx.m_lane = cx.m_strip + Q * lane;
-  const bool hedge = cx.m_strip < 0 || cx.m_strip + Q * kLaneCount > a.cols;
-  cx.n0 = a.row_begin + seg * a.seg_rows;
-  cx.n1 = min(cx.n0 + a.seg_rows, a.row_end);
-  cx.first = max(0, cx.n0 - G::up);
-  const int last_load = min(a.rows - 1, cx.n1 - 1 + G::down);
-  const int last_tick = cx.n1 - 1 + G::down;
+  // This warp's share of the flat (item, strip, row) space: equal work for
+  // every resident warp, so the launch is exactly one wave with no tail.
+  const int rows_out = a.row_end - a.row_begin;
+  const int64_t total = static_cast<int64_t>(a.batch) * a.n_strips * rows_out;
+  int64_t f = total * gw / a.n_warps;
+  const int64_t f_end = total * (gw + 1) / a.n_warps;
 
   Src src;
   src.ring = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(warp) * STAGES * Src::kStageElems;
   src.bars = reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(WARPS) * STAGES * Src::kStageElems * sizeof(T)) +
              warp * STAGES;
-  src.first = cx.first;
-  src.last_load = last_load;
   src.lane = lane;
-  src.m_lane = cx.m_lane;
-  src.m_strip = cx.m_strip;
   src.cols = a.cols;
-  src.b = b;
-  src.boff = static_cast<int64_t>(b) * a.in_bstride;
-  src.start(a, &tmap0, &tmap1, &tmap2, &tmap3);
+  src.init_barriers();
 
-  Sink sink;
-  sink.init(a, static_cast<int64_t>(b) * a.out_bstride, cx.m_lane, max(strip * a.strip_w, 0),
-            min(strip * a.strip_w + a.strip_w, a.cols));
-
-  // Window rows above the segment's first loaded row only ever feed rows that
-  // are not stored; start them at zero so nothing uninitialised is read.
-  Pipe pipe{};
-
-  // Steady range: every stage interior, every row loaded and stored.
-  const int steady_lo = G::down + max(cx.n0, G::kMaxUp);
-  const int steady_hi = min(a.rows - 1, cx.n1 - 1 + G::down);
 #pragma unroll 1
-  for (int t = cx.first; t <= last_tick;) {
-    if (t >= steady_lo && t % kP == 0 && t + kP - 1 <= steady_hi) {
-      if (hedge)
-        steady_chunk<true, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, Phases{});
-      else
-        steady_chunk<false, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, Phases{});
-      t += kP;
-    } else {
-      T row[4][Q];
-      if (t <= last_load) {
-        src.next(row, a, &tmap0, &tmap1, &tmap2, &tmap3);
+  while (f < f_end) {
+    const int64_t column = f / rows_out;  // (item, strip)
+    const int r = static_cast<int>(f - column * rows_out);
+    const int64_t rest = f_end - f;
+    const int seg_len = rest < rows_out - r ? static_cast<int>(rest) : rows_out - r;
+    f += seg_len;
+    const int strip = static_cast<int>(column % a.n_strips);
+    const int b = static_cast<int>(column / a.n_strips);
+
+    Ctx cx;
+    cx.rows = a.rows;
+    cx.cols = a.cols;
+    cx.m_strip = strip * a.strip_w - a.halo_l;
+    cx.m_lane = cx.m_strip + Q * lane;
+    const bool hedge = cx.m_strip < 0 || cx.m_strip + Q * kLaneCount > a.cols;
+    cx.n0 = a.row_begin + r;
+    cx.n1 = cx.n0 + seg_len;
+    cx.first = max(0, cx.n0 - G::up);
+    const int last_load = min(a.rows - 1, cx.n1 - 1 + G::down);
+    const int last_tick = cx.n1 - 1 + G::down;
+
+    src.first = cx.first;
+    src.last_load = last_load;
+    src.m_lane = cx.m_lane;
+    src.m_strip = cx.m_strip;
+    src.b = b;
+    src.boff = static_cast<int64_t>(b) * a.in_bstride;
+    src.start(a, &tmap0, &tmap1, &tmap2, &tmap3);
+
+    Sink sink;
+    sink.init(a, static_cast<int64_t>(b) * a.out_bstride, cx.m_lane, max(strip * a.strip_w, 0),
+              min(strip * a.strip_w + a.strip_w, a.cols));
+
+    // Window rows above the segment's first loaded row only ever feed rows
+    // that are not stored; start them at zero so nothing uninitialised is read.
+    Pipe pipe{};
+
+    // Steady range: every stage interior, every row loaded and stored.
+    const int steady_lo = G::down + max(cx.n0, G::kMaxUp);
+    const int steady_hi = min(a.rows - 1, cx.n1 - 1 + G::down);
+#pragma unroll 1
+    for (int t = cx.first; t <= last_tick;) {
+      if (t >= steady_lo && t % kP == 0 && t + kP - 1 <= steady_hi) {
+        if (hedge)
+          steady_chunk<true, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, Phases{});
+        else
+          steady_chunk<false, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, Phases{});
+        t += kP;
       } else {
+        T row[4][Q];
+        if (t <= last_load) {
+          src.next(row, a, &tmap0, &tmap1, &tmap2, &tmap3);
+        } else {
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+          for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int q = 0; q < Q; ++q) row[c][q] = T(0);
+            for (int q = 0; q < Q; ++q) row[c][q] = T(0);
+        }
+        if (hedge)
+          checked_tick<kP, true>(pipe, row, t, cx, a, sink, Phases{});
+        else
+          checked_tick<kP, false>(pipe, row, t, cx, a, sink, Phases{});
+        ++t;
       }
-      if (hedge)
-        checked_tick<kP, true>(pipe, row, t, cx, a, sink, Phases{});
-      else
-        checked_tick<kP, false>(pipe, row, t, cx, a, sink, Phases{});
-      ++t;
     }
+    src.finish();
   }
-  if constexpr (!kTma) cp_async_wait<0>();
 }
 
 }  // namespace b2dwt

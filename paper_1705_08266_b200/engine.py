@@ -420,6 +420,12 @@ class Transform:
             "dwt",
         )
 
+    def capture_dwt(self, x, levels: int):
+        """Capture the whole ``levels``-deep pyramid of the device image ``x``
+        into a CUDA graph (one host submission per pyramid).  Returns a
+        :class:`PyramidGraph`; write new pixels into ``x`` and ``replay()``."""
+        return PyramidGraph(self, x, levels)
+
     def idwt(self, ll, details, out=None, stream=None):
         torch = self._check(ll, "ll")
         levels = len(details)
@@ -439,6 +445,32 @@ class Transform:
             "idwt",
         )
         return out
+
+
+class PyramidGraph:
+    """A multi-level forward transform captured as one CUDA graph.
+
+    The graph bakes in the device addresses of ``x`` and of the outputs
+    (``ll``, ``details``), which it owns; each :meth:`replay` recomputes the
+    pyramid of whatever ``x`` holds."""
+
+    def __init__(self, tr: Transform, x, levels: int):
+        torch = tr._check(x, "x")
+        h, w = x.shape
+        self.x = x
+        self.ll, self.details = tr.dwt(x, levels)  # allocates + warms up every level
+        self.scratch = torch.empty(((h // 2) * (w // 2) + (h // 4) * (w // 4),), dtype=x.dtype, device=x.device) \
+            if levels > 1 else None
+        tr.dwt_into(x, levels, self.details, self.ll, self.scratch)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            tr.dwt_into(x, levels, self.details, self.ll, self.scratch)
+        self.levels = levels
+
+    def replay(self):
+        self.graph.replay()
+        return self.ll, self.details
 
 
 _TRANSFORMS: dict = {}
