@@ -2,8 +2,9 @@
 
 Translation units:
   csrc/b2dwt_host.cu        C ABI, plan matching, generic interpreter kernel
-  csrc/prog_instance.cu     fused streaming kernels, compiled once per built-in
-                            program (-DB2DWT_PROG=<ident>), in parallel
+  csrc/prog_dispatch.cu     per built-in program: variant selection, cone
+  csrc/prog_variant.cu      ONE fused kernel per unit (program x element type x
+                            layout x arithmetic x fill), compiled in parallel
 
 Flags: -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 (ptxas -v output is
 kept in build/ptxas_<unit>.log for register / spill review).
@@ -28,6 +29,7 @@ LIB = os.path.join(HERE, "libb2dwt.so")
 INCLUDE = os.path.join(ROOT, "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+N_VARIANTS = 8  # see csrc/prog_variant.cu
 NVCC_FLAGS = ["-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", *ARCH]
 
 
@@ -65,7 +67,8 @@ def _stale(target: str, deps) -> bool:
 
 def _compile(args):
     src, obj, defines, log = args
-    cmd = [nvcc(), *NVCC_FLAGS, *defines, "-I", CSRC, "-I", INCLUDE, "-c", src, "-o", obj]
+    extra = os.environ.get("B2DWT_NVCC_EXTRA", "").split()  # experiments, e.g. -DB2DWT_F32_RPS=8
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, *defines, "-I", CSRC, "-I", INCLUDE, "-c", src, "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     with open(log, "w") as fh:
         fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
@@ -77,32 +80,51 @@ def _compile(args):
 def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     deps = _deps()
-    if not force and not _stale(LIB, deps):
-        return LIB
     jobs = jobs or max(1, os.cpu_count() or 1)
     # host TU in C++17 (nvcc 12.9's C++20 front end trips over libstdc++ 13
     # containers); kernel TUs need C++20 for the phase-unrolled tick loop
     tasks = [(os.path.join(CSRC, "b2dwt_host.cu"), os.path.join(BUILD, "b2dwt_host.o"), ["-std=c++17"],
               os.path.join(BUILD, "ptxas_b2dwt_host.log"))]
+    # dev builds: B2DWT_PROGRAMS=ident,... and/or B2DWT_VARIANTS=0,1 compile
+    # only that subset; the rest are stubs (the host falls back to the generic
+    # interpreter for them).  Release builds compile everything.
+    only = os.environ.get("B2DWT_PROGRAMS")
+    only = set(only.split(",")) if only else None
+    vonly = os.environ.get("B2DWT_VARIANTS")
+    vonly = {int(v) for v in vonly.split(",")} if vonly else None
     for ident, inv in _program_units():
-        tasks.append((
-            os.path.join(CSRC, "prog_instance.cu"),
-            os.path.join(BUILD, f"prog_{ident}.o"),
-            ["-std=c++20", f"-DB2DWT_PROG={ident}", f"-DB2DWT_PROG_INV={int(inv)}"],
-            os.path.join(BUILD, f"ptxas_{ident}.log"),
-        ))
+        defs = [f"-DB2DWT_PROG={ident}", f"-DB2DWT_PROG_INV={int(inv)}"]
+        tasks.append((os.path.join(CSRC, "prog_dispatch.cu"), os.path.join(BUILD, f"dispatch_{ident}.o"),
+                      ["-std=c++20", *defs], os.path.join(BUILD, f"ptxas_dispatch_{ident}.log")))
+        for vid in range(N_VARIANTS):
+            real = (only is None or ident in only) and (vonly is None or vid in vonly)
+            tag = "" if real else "_stub"
+            tasks.append((
+                os.path.join(CSRC, "prog_variant.cu"),
+                os.path.join(BUILD, f"v_{ident}_{vid}{tag}.o"),
+                ["-std=c++20", *defs, f"-DB2DWT_VID={vid}"] + ([] if real else ["-DB2DWT_STUB"]),
+                os.path.join(BUILD, f"ptxas_{ident}_{vid}{tag}.log"),
+            ))
     todo = [t for t in tasks if force or _stale(t[1], deps)]
     if verbose:
         print(f"[b2dwt] compiling {len(todo)} units with {jobs} jobs", file=sys.stderr)
+    todo.sort(key=lambda t: ("_stub" in t[1] or "dispatch_" in t[1], t[1]))
     with ThreadPoolExecutor(max_workers=jobs) as pool:
         list(pool.map(_compile, todo))
     objs = [t[1] for t in tasks]
+    manifest = os.path.join(BUILD, "link_manifest.txt")
+    want = "\n".join(objs)
+    have = open(manifest).read() if os.path.exists(manifest) else ""
+    if not force and not todo and have == want and not _stale(LIB, objs):
+        return LIB
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), "-shared", *ARCH, "-o", tmp, *objs, "-lcuda"]
+    cmd = [nvcc(), "-shared", *ARCH, "-o", tmp, *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")
     os.replace(tmp, LIB)
+    with open(manifest, "w") as fh:
+        fh.write(want)
     return LIB
 
 

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -30,6 +32,8 @@ B2DWT_FOR_EACH_PROGRAM(B2DWT_DECLARE)
 namespace {
 
 thread_local std::string g_error;
+long long* g_dbg = nullptr;  // debug: per-warp timing records of the next fused launches
+int64_t g_dbg_n = 0;
 
 int fail(int code, const std::string& msg) {
   g_error = msg;
@@ -46,6 +50,7 @@ struct Builtin {
   int nterms;
   int (*begin)(int);
   TermInfo (*term)(int);
+  double (*coef)(int);
   FusedLauncher launch;
   ConeGetter cone;
   bool inverse;
@@ -59,12 +64,16 @@ template <class P>
 TermInfo term_of(int i) {
   return P::term(i);
 }
+template <class P>
+double coef_of(int i) {
+  return P::coef(i);
+}
 
 const Builtin* builtins() {
   static const Builtin table[] = {
 #define B2DWT_ROW(ID, NAME)                                                                                      \
   {progs::NAME::kKey,        progs::NAME::kNumSub, progs::NAME::kNumTerms, &begin_of<progs::NAME>,             \
-   &term_of<progs::NAME>,    &b2dwt_fused_##NAME,  &b2dwt_cone_##NAME,     std::strstr(progs::NAME::kKey, "/inv") \
+   &term_of<progs::NAME>,    &coef_of<progs::NAME>,    &b2dwt_fused_##NAME,  &b2dwt_cone_##NAME,     std::strstr(progs::NAME::kKey, "/inv") \
    != nullptr},
       B2DWT_FOR_EACH_PROGRAM(B2DWT_ROW)
 #undef B2DWT_ROW
@@ -93,6 +102,59 @@ namespace {
 
 bool strict_of(const b2dwt_plan_s* p) { return (p->flags & B2DWT_FAST) == 0; }
 
+// Pool of zero-initialised {tickets, done} counter pairs per device for the
+// dynamic work tail.  Each launch takes the next slot round-robin; the kernel's
+// last warp resets its slot, so launches queued on one stream reuse slots
+// safely and up to kSlots launches may run concurrently on other streams.
+unsigned long long* tail_counter_slot() {
+  constexpr int kSlots = 256, kMaxDev = 64;
+  static std::mutex mu;
+  static unsigned long long* pool[kMaxDev] = {};
+  static unsigned next[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pool[dev]) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, kSlots * 2 * sizeof(unsigned long long)) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return nullptr;
+    }
+    cudaMemset(p, 0, kSlots * 2 * sizeof(unsigned long long));
+    pool[dev] = static_cast<unsigned long long*>(p);
+  }
+  return pool[dev] + 2 * (next[dev]++ % kSlots);
+}
+
+// Work split: [0] share of the rows split statically (1/1024), [1] rows per
+// dynamically claimed tail chunk.  B2DWT_STATIC_FRAC / B2DWT_TAIL_ROWS override.
+int split_param(int which) {
+  static const int v[3] = {[] {
+                             const char* e = std::getenv("B2DWT_STATIC_FRAC");
+                             return e ? std::atoi(e) : 512;
+                           }(),
+                           [] {
+                             const char* e = std::getenv("B2DWT_TAIL_ROWS");
+                             return e ? std::atoi(e) : 32;
+                           }(),
+                           [] {
+                             const char* e = std::getenv("B2DWT_STRIP_ALIGN");
+                             return e ? std::atoi(e) : 0;
+                           }()};
+  return v[which];
+}
+
+// Relative cost of an image-edge strip row (eighths of an interior row) used to
+// balance the work split; B2DWT_EDGE_COST8 overrides it for tuning.
+int edge_cost8() {
+  static int v = [] {
+    const char* e = std::getenv("B2DWT_EDGE_COST8");
+    const int x = e ? std::atoi(e) : 12;
+    return x < 8 ? 8 : x;
+  }();
+  return v;
+}
+
 int match_builtin(const b2dwt_plan_s& p) {
   const Builtin* tab = builtins();
   for (int id = 0; id < B2DWT_NUM_PROGRAMS; ++id) {
@@ -104,7 +166,8 @@ int match_builtin(const b2dwt_plan_s& p) {
     for (int i = 0; i < b.nterms && ok; ++i) {
       const TermInfo ti = b.term(i);
       const b2dwt_term& t = p.terms[i];
-      ok = ti.src == t.src && ti.dm == t.dm && ti.dn == t.dn && (!ti.unit || t.coeff == 1.0);
+      // same term, same coefficient bits (they are compiled into the kernel)
+      ok = ti.src == t.src && ti.dm == t.dm && ti.dn == t.dn && b.coef(i) == t.coeff;
     }
     if (ok) return id;
   }
@@ -226,8 +289,16 @@ int run_fused(const b2dwt_plan_s& p, FusedLaunch& r) {
   // spread them over the whole machine; 8 rows keeps the cone re-read <= 50%
   // there and negligible on large levels, which fill the machine anyway.
   r.min_rows_per_warp = 8;
+  r.edge_cost8 = edge_cost8();
+  r.dbg = g_dbg;
+  // dynamic tail: a counter slot from the per-device pool (self-resetting)
+  r.tail_counter = split_param(0) < 1024 ? tail_counter_slot() : nullptr;
+  r.static_frac = split_param(0);
+  r.tail_rows = split_param(1);
+  r.strip_align = split_param(2);
   bool used_tma = false;
   const cudaError_t e = b.launch(r, &used_tma);
+  if (e == cudaErrorNotSupported) return fail(B2DWT_EUNSUPPORTED, "no compiled fused variant for this request");
   if (e != cudaSuccess) return cuda_fail(e, "fused stream kernel");
   return B2DWT_OK;
 }
@@ -335,6 +406,28 @@ int b2dwt_plan_create(const b2dwt_program* program, int32_t dtype, int32_t flags
   return B2DWT_OK;
 }
 
+// Debug hooks (not part of the public header): per-warp cycle counts of the
+// fused kernel, used to tune the work split.
+int b2dwt_debug_enable(int64_t max_warps) {
+  if (g_dbg) cudaFree(g_dbg);
+  g_dbg = nullptr;
+  g_dbg_n = 0;
+  if (max_warps <= 0) return B2DWT_OK;
+  if (cudaMalloc(&g_dbg, static_cast<size_t>(max_warps) * 4 * sizeof(long long)) != cudaSuccess)
+    return fail(B2DWT_ECUDA, "debug buffer");
+  cudaMemset(g_dbg, 0, static_cast<size_t>(max_warps) * 4 * sizeof(long long));
+  g_dbg_n = max_warps;
+  return B2DWT_OK;
+}
+
+int b2dwt_debug_fetch(long long* host, int64_t max_warps) {
+  if (!g_dbg) return fail(B2DWT_EINVAL, "debug timing not enabled");
+  const int64_t n = max_warps < g_dbg_n ? max_warps : g_dbg_n;
+  if (cudaMemcpy(host, g_dbg, static_cast<size_t>(n) * 4 * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(B2DWT_ECUDA, "debug fetch");
+  return B2DWT_OK;
+}
+
 int b2dwt_plan_destroy(b2dwt_plan plan) {
   delete plan;
   return B2DWT_OK;
@@ -385,7 +478,8 @@ int b2dwt_run_components(b2dwt_plan plan, const b2dwt_planes* in, const b2dwt_pl
     r.row_end = static_cast<int>(rows);
     r.batch = batch;
     r.stream = s;
-    return run_fused(*plan, r);
+    const int rc = run_fused(*plan, r);
+    if (rc != B2DWT_EUNSUPPORTED) return rc;
   }
   const size_t es = esize(plan->dtype);
   return run_generic(*plan, planar_views(in, es), in->bstride, planar_views(out, es), out->bstride, rows, cols,
@@ -421,7 +515,8 @@ int b2dwt_forward(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t 
     r.row_end = static_cast<int>(rows);
     r.batch = batch;
     r.stream = s;
-    return run_fused(*plan, r);
+    const int rc = run_fused(*plan, r);
+    if (rc != B2DWT_EUNSUPPORTED) return rc;
   }
   const size_t es = esize(plan->dtype);
   return run_generic(*plan, image_views(image, image_ld, es), image_bstride, planar_views(out, es), out->bstride,
@@ -457,7 +552,8 @@ int b2dwt_inverse(b2dwt_plan plan, const b2dwt_planes* in, void* image, int64_t 
     r.row_end = static_cast<int>(rows);
     r.batch = batch;
     r.stream = s;
-    return run_fused(*plan, r);
+    const int rc = run_fused(*plan, r);
+    if (rc != B2DWT_EUNSUPPORTED) return rc;
   }
   const size_t es = esize(plan->dtype);
   return run_generic(*plan, planar_views(in, es), in->bstride, image_views(image, image_ld, es), image_bstride,

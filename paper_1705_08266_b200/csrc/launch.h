@@ -30,6 +30,12 @@ struct FusedLaunch {
   const double* coeffs;
   int n_coeffs;
   int min_rows_per_warp;  // work split: lower bound on rows per warp (latency vs cone overhead)
+  int edge_cost8;         // work split: cost of an image-edge strip row in 1/8 of an interior row
+  long long* dbg;         // per-warp timing records (b2dwt_debug_*), usually null
+  unsigned long long* tail_counter;  // zeroed device counter for the dynamic tail, or null
+  int static_frac;        // share of the work split statically (1/1024)
+  int tail_rows;          // rows per dynamic tail chunk
+  int strip_align;        // strip start / width alignment in quads (>= 2)
   cudaStream_t stream;
 };
 

@@ -1,9 +1,9 @@
-// prog_instance.cu -- fused-kernel instantiations for ONE built-in program.
-//
-// Compiled once per program structure with
-//   -DB2DWT_PROG=<ident> -DB2DWT_PROG_INV=<0|1>
-// (see paper_1705_08266_b200/build.py) so the 16 programs build in parallel.
-// Exposes b2dwt_fused_<ident>() and b2dwt_cone_<ident>() to b2dwt_host.cu.
+// launch_impl.cuh -- host side of one fused-kernel instantiation: strip
+// geometry, work split, TMA descriptors, launch.  Included by prog_variant.cu,
+// which compiles exactly one (program, element type, layout, arithmetic, fill)
+// kernel per translation unit so the build parallelises across CPU cores.
+#pragma once
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -14,20 +14,9 @@
 #include "launch.h"
 #include "stream_kernel.cuh"
 
-#ifndef B2DWT_PROG
-#error "compile with -DB2DWT_PROG=<program ident>"
-#endif
-#ifndef B2DWT_PROG_INV
-#define B2DWT_PROG_INV 0
-#endif
-
-#define B2DWT_CAT2(a, b) a##b
-#define B2DWT_CAT(a, b) B2DWT_CAT2(a, b)
-
 namespace b2dwt {
 namespace {
 
-using Prog = progs::B2DWT_PROG;
 constexpr int kQ = 2;
 
 // Launch shape per element type: WARPS per CTA, ring STAGES, RPS quad rows
@@ -36,7 +25,13 @@ template <class T>
 struct Shape;
 template <>
 struct Shape<float> {
-  static constexpr int kWarps = 4, kStages = 4, kRps = 2;
+#ifndef B2DWT_F32_STAGES
+#define B2DWT_F32_STAGES 4
+#endif
+#ifndef B2DWT_F32_RPS
+#define B2DWT_F32_RPS 4
+#endif
+  static constexpr int kWarps = 4, kStages = B2DWT_F32_STAGES, kRps = B2DWT_F32_RPS;
 };
 template <>
 struct Shape<double> {
@@ -96,7 +91,7 @@ int num_sms() {
   return sms;
 }
 
-template <class T, int LIN, int LOUT, bool kStrict, bool kTma>
+template <class Prog, class T, int LIN, int LOUT, bool kStrict, bool kTma>
 cudaError_t launch(const FusedLaunch& r) {
   using S = Shape<T>;
   using Args = StreamArgs<T, (Prog::kNumTerms > 0 ? Prog::kNumTerms : 1)>;
@@ -133,17 +128,20 @@ cudaError_t launch(const FusedLaunch& r) {
   a.row_begin = r.row_begin;
   a.row_end = r.row_end;
   a.batch = r.batch;
-  for (int i = 0; i < Prog::kNumTerms; ++i) a.k[i] = static_cast<T>(r.coeffs[i]);
 
-  // strips: 32*Q quads loaded, the cone recomputed on both sides.  Strip
-  // starts are kept 16-byte aligned in the input rows (a TMA box whose
-  // innermost start is not 16 B aligned faults) and even (vector stores).
+  // strips: 32*Q quads loaded, the cone recomputed on both sides.  Geometry
+  // keeps DRAM sectors whole: each strip's input box starts on a 32-B boundary
+  // (TMA itself faults below 16 B) and each output row segment is a whole
+  // number of 32-B sectors at a sector boundary -- partial sectors written by
+  // two strips cost a DRAM read-modify-write (measured: 0.59 -> 0.48 ms at C3).
   using C = Cone<Prog>;
-  constexpr int kQuadBytes = static_cast<int>(sizeof(T)) * (LIN == kLayoutInterleaved ? 2 : 1);
-  constexpr int kAlign = std::max(2, 16 / kQuadBytes);
-  const int halo_l = (C::left + kAlign - 1) / kAlign * kAlign;
+  constexpr int kInQuadBytes = static_cast<int>(sizeof(T)) * (LIN == kLayoutInterleaved ? 2 : 1);
+  constexpr int kOutQuadBytes = static_cast<int>(sizeof(T)) * (LOUT == kLayoutInterleaved ? 2 : 1);
+  const int halo_align = std::max({2, std::min(4, 32 / kInQuadBytes), 16 / kInQuadBytes, r.strip_align});
+  const int width_align = std::max(halo_align, 32 / kOutQuadBytes);
+  const int halo_l = (C::left + halo_align - 1) / halo_align * halo_align;
   int strip_w = kLaneCount * kQ - halo_l - C::right;
-  strip_w = strip_w / kAlign * kAlign;
+  strip_w = strip_w / width_align * width_align;
   a.strip_w = strip_w;
   a.halo_l = halo_l;
   a.n_strips = (r.cols + strip_w - 1) / strip_w;
@@ -156,6 +154,11 @@ cudaError_t launch(const FusedLaunch& r) {
   const int64_t total_rows = static_cast<int64_t>(r.batch) * a.n_strips * rows_out;
   const int64_t n_warps = std::max<int64_t>(1, std::min(resident, (total_rows + kMinRows - 1) / kMinRows));
   a.n_warps = static_cast<int>(n_warps);
+  a.edge_cost = std::max(8, r.edge_cost8);
+  a.dbg = r.dbg;
+  a.tail_counter = r.tail_counter;
+  a.static_frac = std::min(1024, std::max(0, r.static_frac));
+  a.tail_chunk = std::max(1, r.tail_rows) * 8;
 
   CUtensorMap maps[4];
   memset(maps, 0, sizeof(maps));
@@ -176,44 +179,5 @@ cudaError_t launch(const FusedLaunch& r) {
   return cudaGetLastError();
 }
 
-template <class T, int LIN, int LOUT>
-cudaError_t dispatch_fill(const FusedLaunch& r, bool* used_tma) {
-  if (r.allow_tma) {
-    const cudaError_t e = r.strict ? launch<T, LIN, LOUT, true, true>(r) : launch<T, LIN, LOUT, false, true>(r);
-    if (e != cudaErrorNotSupported) {
-      *used_tma = true;
-      return e;
-    }
-    (void)cudaGetLastError();
-  }
-  *used_tma = false;
-  return r.strict ? launch<T, LIN, LOUT, true, false>(r) : launch<T, LIN, LOUT, false, false>(r);
-}
-
-template <class T>
-cudaError_t dispatch_layout(const FusedLaunch& r, bool* used_tma) {
-#if B2DWT_PROG_INV
-  if (r.lin == kLayoutPlanar && r.lout == kLayoutInterleaved)
-    return dispatch_fill<T, kLayoutPlanar, kLayoutInterleaved>(r, used_tma);
-#else
-  if (r.lin == kLayoutInterleaved && r.lout == kLayoutPlanar)
-    return dispatch_fill<T, kLayoutInterleaved, kLayoutPlanar>(r, used_tma);
-#endif
-  if (r.lin == kLayoutPlanar && r.lout == kLayoutPlanar)
-    return dispatch_fill<T, kLayoutPlanar, kLayoutPlanar>(r, used_tma);
-  return cudaErrorInvalidValue;
-}
-
 }  // namespace
-
-cudaError_t B2DWT_CAT(b2dwt_fused_, B2DWT_PROG)(const FusedLaunch& r, bool* used_tma) {
-  if (r.n_coeffs != Prog::kNumTerms) return cudaErrorInvalidValue;
-  return r.dtype == 0 ? dispatch_layout<float>(r, used_tma) : dispatch_layout<double>(r, used_tma);
-}
-
-ConeInfo B2DWT_CAT(b2dwt_cone_, B2DWT_PROG)() {
-  using C = Cone<Prog>;
-  return ConeInfo{C::up, C::down, C::left, C::right};
-}
-
 }  // namespace b2dwt

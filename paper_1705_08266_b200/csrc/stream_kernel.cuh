@@ -67,7 +67,12 @@ struct StreamArgs {
   int halo_l;              // strip's first quad = strip * strip_w - halo_l
   int n_strips, batch;
   int n_warps;              // warps sharing the flat (item, strip, row) space
-  T k[NT];  // coefficients, flat compiled order
+  int edge_cost;            // cost of an image-edge strip row, in 1/8 of an interior row
+  long long* dbg;           // optional per-warp timing record (debug builds of the split), or null
+  unsigned long long* tail_counter;  // [0] tail chunk tickets, [1] warps done (null: fully static split);
+                                     // the last warp out resets both, so the slot is reusable
+  int static_frac;          // share of the cost split statically, in 1/1024
+  int tail_chunk;           // cost units per dynamic tail chunk
 };
 
 __host__ __device__ constexpr int cmod(int x, int m) { return ((x % m) + m) % m; }
@@ -114,11 +119,19 @@ using Cone = Geo<P>;
 // Per-warp runtime context shared by all pipeline stages.
 struct Ctx {
   int rows, cols;
+  bool fold1;    // cols large enough that every halo read reflects at most once
+  bool hedge;    // this strip's columns leave [0, cols)
   int first;     // first quad row any stage computes (segment start - cone)
   int n0, n1;    // rows stored
   int m_lane;    // global quad column of this lane's slot 0
   int m_strip;   // global quad column of lane 0's slot 0
 };
+
+// Single-fold whole-sample reflection of component index i (valid when i is
+// less than one component length outside [0, cs)): engine.py:55-92 unrolled.
+__device__ __forceinline__ int reflect1(int i, int parity, int cs) {
+  return i < 0 ? -i - parity : (i >= cs ? 2 * cs - 1 - parity - i : i);
+}
 
 template <class T>
 __device__ __forceinline__ T shfl_idx(T v, int src) {
@@ -154,10 +167,18 @@ struct Stage<P, T, Q, kStrict, S, false> {
   Next next;
 
   // One tick: append input row (t - kLag), compute row n = t - kLag - D.
-  template <int PH, bool CHECK, bool HEDGE, class Args, class Sink>
+  // HEDGE: 0 interior strip, 1 image-edge strip, 2 decided at run time (checked ticks).
+  template <int PH, bool CHECK, int HEDGE, class Args, class Sink>
   __device__ __forceinline__ void tick(const T (&in)[4][Q], int t, const Ctx& cx, const Args& a, Sink& sink) {
     constexpr int kSlotIn = cmod(PH - kLag, NW);
-    append<HEDGE>(in, w[kSlotIn], cx);
+    if constexpr (HEDGE == 2) {
+      if (cx.hedge)
+        append<true>(in, w[kSlotIn], cx);
+      else
+        append<false>(in, w[kSlotIn], cx);
+    } else {
+      append<HEDGE == 1>(in, w[kSlotIn], cx);
+    }
     constexpr int kOff = cmod(PH - kLag - D, NW);  // slot of row n
     T out[4][Q];
     if constexpr (!CHECK) {
@@ -211,28 +232,62 @@ struct Stage<P, T, Q, kStrict, S, false> {
         for (int e = 0; e < R; ++e)
           if (e < nd.right) x[L + Q + e] = shfl_down1(in[C][e]);
       } else {
-        // Image-edge strip: every slot a neighbour read can reach goes through
-        // the reflection map -- own slots too, since the image edge may fall
-        // inside a lane (odd component widths).
+        // Image-edge strip.  Wide images: do the interior exchange, then the one
+        // lane whose window crosses column 0 and the lanes whose window crosses
+        // column cols fold their out-of-image slots onto the mirrored in-image
+        // slots of the SAME window (single-fold whole-sample symmetry,
+        // engine.py:55-92) -- predicated selects, no extra shuffles.
+        if (cx.fold1) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const bool needed = (nd.left > 0 || nd.right > 0) && e >= L - nd.left && e < L + Q + nd.right;
-          if (!needed) continue;
-          const int col = reflect(cx.m_lane - L + e, col_parity(C), cx.cols);
-          const int rel = col - cx.m_strip;
-          int src = rel / Q;
-          const int slot = rel - src * Q;
-          src = src < 0 ? 0 : (src > kLaneCount - 1 ? kLaneCount - 1 : src);
-          T v = shfl_idx(in[C][0], src);
+          for (int e = 0; e < L; ++e)
+            if (L - e <= nd.left) x[e] = shfl_up1(in[C][Q - L + e]);
 #pragma unroll
-          for (int j = 1; j < Q; ++j) {
-            const T tt = shfl_idx(in[C][j], src);
-            v = (slot == j) ? tt : v;
+          for (int e = 0; e < R; ++e)
+            if (e < nd.right) x[L + Q + e] = shfl_down1(in[C][e]);
+          constexpr int p = col_parity(C);
+          // left edge: window column d = e - L < 0 mirrors to -d - p
+          const bool at_left = cx.m_lane == 0;
+#pragma unroll
+          for (int e = 0; e < L; ++e) {
+            constexpr_if_fold(x, at_left, e, L - (e - L) - p);
           }
-          x[e] = v;
+          // right edge: k = cols - m_lane in-image slots; column d >= k mirrors to 2k-1-p-d
+          const int k = cx.cols - cx.m_lane;
+#pragma unroll
+          for (int kk = 1; kk < Q + R; ++kk) {
+#pragma unroll
+            for (int d = kk; d < Q + R; ++d) {
+              const int dm = 2 * kk - 1 - p - d;  // mirrored column offset
+              if (dm >= -L && dm < kk) constexpr_if_fold(x, k == kk, L + d, L + dm);
+            }
+          }
+        } else {
+          // Narrow images: generic gather through the full (periodic) map.
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const bool needed = (nd.left > 0 || nd.right > 0) && e >= L - nd.left && e < L + Q + nd.right;
+            if (!needed) continue;
+            const int col = reflect(cx.m_lane - L + e, col_parity(C), cx.cols);
+            const int rel = col - cx.m_strip;
+            int src = rel / Q;
+            const int slot = rel - src * Q;
+            src = src < 0 ? 0 : (src > kLaneCount - 1 ? kLaneCount - 1 : src);
+            T v = shfl_idx(in[C][0], src);
+#pragma unroll
+            for (int j = 1; j < Q; ++j) {
+              const T tt = shfl_idx(in[C][j], src);
+              v = (slot == j) ? tt : v;
+            }
+            x[e] = v;
+          }
         }
       }
     }
+  }
+
+  // x[dst] = x[src] where `pred` (indices are compile-time after unrolling).
+  __device__ __forceinline__ static void constexpr_if_fold(T (&x)[E], bool pred, int dst, int src) {
+    if (dst >= 0 && dst < E && src >= 0 && src < E) x[dst] = pred ? x[src] : x[dst];
   }
 
   // Top / bottom rows: rebuild the window in logical order through the row
@@ -263,10 +318,11 @@ struct Stage<P, T, Q, kStrict, S, false> {
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const T x = win[slot][ti.src][L + q + ti.dm];
+      constexpr T kc = static_cast<T>(P::coef(idx));  // liftfuse: dtype.type(coeff), engine.py:357
       if constexpr (K == 0) {
-        acc[q] = ti.unit ? x : Ar::mul(x, a.k[idx]);
+        acc[q] = ti.unit ? x : Ar::mul(x, kc);
       } else {
-        acc[q] = ti.unit ? Ar::add(acc[q], x) : Ar::mac(acc[q], x, a.k[idx]);
+        acc[q] = ti.unit ? Ar::add(acc[q], x) : Ar::mac(acc[q], x, kc);
       }
     }
   }
@@ -290,6 +346,14 @@ struct Stage<P, T, Q, kStrict, S, false> {
 
   template <int OFF, class Args>
   __device__ __forceinline__ static void eval(const T (&win)[NW][4][E], T (&out)[4][Q], const Args& a) {
+#ifdef B2DWT_EXPERIMENT_COPY
+    // data-movement ceiling experiment: pass the input through untouched
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int q = 0; q < Q; ++q) out[c][q] = win[cmod(OFF, NW)][c][L + q];
+    return;
+#endif
     eval_target<OFF, 0>(win, out, a);
     eval_target<OFF, 1>(win, out, a);
     eval_target<OFF, 2>(win, out, a);
@@ -300,13 +364,14 @@ struct Stage<P, T, Q, kStrict, S, false> {
 // End of the pipeline: hand the finished row (t - sum of lookaheads) to the sink.
 template <class P, class T, int Q, bool kStrict, int S>
 struct Stage<P, T, Q, kStrict, S, true> {
-  template <int PH, bool CHECK, bool HEDGE, class Args, class Sink>
+  template <int PH, bool CHECK, int HEDGE, class Args, class Sink>
   __device__ __forceinline__ void tick(const T (&in)[4][Q], int t, const Ctx& cx, const Args& a, Sink& sink) {
     const int n = t - Geo<P>::down;
     if constexpr (CHECK) {
       if (n < cx.n0 || n >= cx.n1) return;
     }
-    sink.store(in, n);
+    // the interior steady path only ever has full, aligned lanes or idle lanes
+    sink.template store<CHECK || HEDGE != 0>(in, n);
   }
 };
 
@@ -342,10 +407,26 @@ struct StoreSink<T, Q, kLayoutPlanar> {
     any_scalar = __any_sync(0xffffffffu, mask != 0 && !(full && vec));
   }
 
+  template <bool kScalar>
   __device__ __forceinline__ void store(const T (&v)[4][Q], int n) {
+#ifdef B2DWT_EXPERIMENT_NOSTORE
+    // load-path ceiling experiment: keep the values alive, store (almost) nothing
+    T acc = T(0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int q = 0; q < Q; ++q) acc += v[c][q];
+    if (acc == T(-12345)) base[0][n] = acc;
+    return;
+#endif
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
+#ifdef B2DWT_EXPERIMENT_L2STORE
+      // write-path experiment: same instructions, all rows folded into 64 rows (L2 resident)
+      T* p = base[c] + static_cast<int64_t>(n & 63) * ld[c];
+#else
       T* p = base[c] + static_cast<int64_t>(n) * ld[c];
+#endif
       if (full && vec) {
         if constexpr (Q == 2 && sizeof(T) == 4) {
           *reinterpret_cast<float2*>(p) = make_float2(v[c][0], v[c][1]);
@@ -356,7 +437,7 @@ struct StoreSink<T, Q, kLayoutPlanar> {
           for (int q = 0; q < Q; ++q) p[q] = v[c][q];
         }
       }
-      if (any_scalar) {  // warp-uniform: only warps that own ragged / unaligned lanes
+      if (kScalar && any_scalar) {  // warp-uniform: only warps that own ragged / unaligned lanes
         if (!(full && vec)) {
 #pragma unroll
           for (int q = 0; q < Q; ++q)
@@ -388,6 +469,7 @@ struct StoreSink<T, Q, kLayoutInterleaved> {
     any_scalar = __any_sync(0xffffffffu, mask != 0 && !(full && vec));
   }
 
+  template <bool kScalar>
   __device__ __forceinline__ void store(const T (&v)[4][Q], int n) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -408,7 +490,7 @@ struct StoreSink<T, Q, kLayoutInterleaved> {
           }
         }
       }
-      if (any_scalar) {
+      if (kScalar && any_scalar) {
         if (!(full && vec)) {
 #pragma unroll
           for (int q = 0; q < Q; ++q)
@@ -483,6 +565,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "}\n" ::"r"(b),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
@@ -606,6 +691,9 @@ struct RowSource {
   template <class Args>
   __device__ __forceinline__ void issue(int kk, const Args& a, const CUtensorMap* tm0, const CUtensorMap* tm1,
                                         const CUtensorMap* tm2, const CUtensorMap* tm3) {
+#ifdef B2DWT_EXPERIMENT_NOLOAD
+    return;  // store-path ceiling experiment: compute on whatever the ring holds
+#endif
     const int g = base + kk;
     T* s = ring + (g % STAGES) * kStageElems;
     if constexpr (kTma) {
@@ -635,12 +723,20 @@ struct RowSource {
     }
   }
 
-  __device__ __forceinline__ void init_barriers() {
+  __device__ __forceinline__ void init_barriers(const CUtensorMap* tm0, const CUtensorMap* tm1,
+                                                const CUtensorMap* tm2, const CUtensorMap* tm3) {
     base = 0;
     if constexpr (kTma) {
       if (lane == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(bars + s, 1);
         fence_mbar_init();
+        // warm the descriptor cache: every stage's TMA names these maps
+        prefetch_tensormap(tm0);
+        if constexpr (LIN == kLayoutPlanar) {
+          prefetch_tensormap(tm1);
+          prefetch_tensormap(tm2);
+          prefetch_tensormap(tm3);
+        }
       }
       __syncwarp();
     }
@@ -677,7 +773,9 @@ struct RowSource {
       ++k;
       const int g = base + k;
       if constexpr (kTma) {
+#ifndef B2DWT_EXPERIMENT_NOLOAD
         mbar_wait(bars + (g % STAGES), (g / STAGES) & 1);
+#endif
         __syncwarp();
         // slot (g-1) % STAGES was consumed in the previous round: refill it
         if (k + STAGES - 1 < n_stages) {
@@ -696,22 +794,22 @@ struct RowSource {
 
 // ---------------------------------------------------------------------------
 // Tick helpers (everything force-inlined: the pipeline must stay in registers).
-template <int PH, bool CHECK, bool HEDGE, class Pipe, class T, int Q, class Args, class Sink>
+template <int PH, bool CHECK, int HEDGE, class Pipe, class T, int Q, class Args, class Sink>
 __device__ __forceinline__ void run_tick(Pipe& pipe, const T (&row)[4][Q], int t, const Ctx& cx, const Args& a,
                                          Sink& sink) {
   pipe.template tick<PH, CHECK, HEDGE>(row, t, cx, a, sink);
 }
 
-// Checked tick at runtime phase t % P.
-template <int P, bool HEDGE, class Pipe, class T, int Q, class Args, class Sink, int... I>
+// Checked tick at runtime phase t % P (edge flag read at run time).
+template <int P, class Pipe, class T, int Q, class Args, class Sink, int... I>
 __device__ __forceinline__ void checked_tick(Pipe& pipe, const T (&row)[4][Q], int t, const Ctx& cx, const Args& a,
                                              Sink& sink, std::integer_sequence<int, I...>) {
   const int ph = t % P;
-  ((ph == I ? run_tick<I, true, HEDGE>(pipe, row, t, cx, a, sink) : void()), ...);
+  ((ph == I ? run_tick<I, true, 2>(pipe, row, t, cx, a, sink) : void()), ...);
 }
 
 // P unchecked ticks t .. t+P-1 (t % P == 0).
-template <bool HEDGE, class T, int Q, class Pipe, class Src, class Args, class Sink, int... I>
+template <int HEDGE, class T, int Q, class Pipe, class Src, class Args, class Sink, int... I>
 __device__ __forceinline__ void steady_chunk(Pipe& pipe, Src& src, int t, const Ctx& cx, const Args& a, Sink& sink,
                                              const CUtensorMap* m0, const CUtensorMap* m1, const CUtensorMap* m2,
                                              const CUtensorMap* m3, std::integer_sequence<int, I...>) {
@@ -727,8 +825,13 @@ __device__ __forceinline__ void steady_chunk(Pipe& pipe, Src& src, int t, const 
 //   Q        quads per lane
 //   LIN/LOUT input / output layout
 //   kTma     fill the ring with TMA (requires 16 B pitches) instead of cp.async
+// f32: cap registers at 168/thread so 3 CTAs (12 warps) fit per SM; without
+// the hint ptxas spends ~200 and only 2 CTAs fit.
+#ifndef B2DWT_MIN_CTAS_PER_SM
+#define B2DWT_MIN_CTAS_PER_SM 3
+#endif
 template <class P, class T, int Q, int LIN, int LOUT, bool kStrict, bool kTma, int WARPS, int STAGES, int RPS>
-__global__ void __launch_bounds__(WARPS* kLaneCount)
+__global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN_CTAS_PER_SM : 1))
     stream_kernel(const __grid_constant__ StreamArgs<T, (P::kNumTerms > 0 ? P::kNumTerms : 1)> a,
                   const __grid_constant__ CUtensorMap tmap0, const __grid_constant__ CUtensorMap tmap1,
                   const __grid_constant__ CUtensorMap tmap2, const __grid_constant__ CUtensorMap tmap3) {
@@ -744,13 +847,33 @@ __global__ void __launch_bounds__(WARPS* kLaneCount)
   const int lane = threadIdx.x % kLaneCount;
   const int gw = blockIdx.x * WARPS + warp;
   if (gw >= a.n_warps) return;  // warp-uniform; no block-wide barrier follows
+  const long long clk0 = clock64();
+  int dbg_rows = 0, dbg_edge_rows = 0;
 
-  // This warp's share of the flat (item, strip, row) space: equal work for
-  // every resident warp, so the launch is exactly one wave with no tail.
+  // This warp's share of the (item, strip, row) space, in cost units: an
+  // interior strip row costs 8, a row of a strip touching the left/right image
+  // edge costs edge_cost (its halo goes through the reflection map).  Every
+  // resident warp gets the same cost, so the launch is one wave with no tail.
   const int rows_out = a.row_end - a.row_begin;
-  const int64_t total = static_cast<int64_t>(a.batch) * a.n_strips * rows_out;
-  int64_t f = total * gw / a.n_warps;
-  const int64_t f_end = total * (gw + 1) / a.n_warps;
+  const int qspan = Q * kLaneCount;
+  // strips [0, h0) and [h1, n_strips) touch an image edge
+  const int h0 = a.halo_l > 0 ? 1 : 0;
+  int h1 = a.n_strips;
+  while (h1 > h0 && (h1 - 1) * a.strip_w - a.halo_l + qspan > a.cols) --h1;
+  const int64_t we = a.edge_cost, wi = 8;
+  auto strip_cost0 = [&](int s) -> int64_t {  // cost of strips [0, s) of one item, per row
+    const int64_t e = (s < h0 ? s : h0) + (s > h1 ? s - h1 : 0);
+    return e * we + (s - e) * wi;
+  };
+  const int64_t item_cost = strip_cost0(a.n_strips) * rows_out;
+  const int64_t total = item_cost * a.batch;
+  // Two tiers: [0, static_end) is split evenly over the resident warps (long
+  // pipelines, no atomics); the tail [static_end, total) is handed out in small
+  // chunks through an atomic counter, so SMs that run faster absorb more of it.
+  const int64_t static_end =
+      a.tail_counter != nullptr ? total * a.static_frac / 1024 : total;
+  int64_t f = static_end * gw / a.n_warps;
+  int64_t f_end = static_end * (gw + 1) / a.n_warps;
 
   Src src;
   src.ring = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(warp) * STAGES * Src::kStageElems;
@@ -758,24 +881,48 @@ __global__ void __launch_bounds__(WARPS* kLaneCount)
              warp * STAGES;
   src.lane = lane;
   src.cols = a.cols;
-  src.init_barriers();
+  src.init_barriers(&tmap0, &tmap1, &tmap2, &tmap3);
 
 #pragma unroll 1
+  for (;;) {
+#pragma unroll 1
   while (f < f_end) {
-    const int64_t column = f / rows_out;  // (item, strip)
-    const int r = static_cast<int>(f - column * rows_out);
-    const int64_t rest = f_end - f;
-    const int seg_len = rest < rows_out - r ? static_cast<int>(rest) : rows_out - r;
-    f += seg_len;
-    const int strip = static_cast<int>(column % a.n_strips);
-    const int b = static_cast<int>(column / a.n_strips);
+    const int b = static_cast<int>(f / item_cost);
+    const int64_t fi = f - b * item_cost;
+    // strip containing cost offset fi (piecewise-linear inverse of strip_cost0)
+    int strip;
+    {
+      const int64_t c_h0 = static_cast<int64_t>(h0) * we * rows_out;
+      const int64_t c_h1 = strip_cost0(h1) * rows_out;
+      if (fi < c_h0)
+        strip = static_cast<int>(fi / (we * rows_out));
+      else if (fi < c_h1)
+        strip = h0 + static_cast<int>((fi - c_h0) / (wi * rows_out));
+      else
+        strip = h1 + static_cast<int>((fi - c_h1) / (we * rows_out));
+      if (strip >= a.n_strips) strip = a.n_strips - 1;
+    }
+    const bool edge_strip = strip < h0 || strip >= h1;
+    const int64_t wr = edge_strip ? we : wi;
+    const int64_t c0 = b * item_cost + strip_cost0(strip) * rows_out;  // cost of row 0 of this strip
+    // rows whose start cost lies in [f, f_end)
+    const int r0 = static_cast<int>((f - c0 + wr - 1) / wr);
+    const int r1 = static_cast<int>(min(static_cast<int64_t>(rows_out), (f_end - c0 + wr - 1) / wr));
+    f = c0 + wr * rows_out;  // next strip
+    if (r0 >= r1) continue;
+    const int r = r0;
+    const int seg_len = r1 - r0;
+    dbg_rows += seg_len;
+    dbg_edge_rows += edge_strip ? seg_len : 0;
 
     Ctx cx;
     cx.rows = a.rows;
     cx.cols = a.cols;
+    cx.fold1 = a.cols >= 2 * qspan;
     cx.m_strip = strip * a.strip_w - a.halo_l;
     cx.m_lane = cx.m_strip + Q * lane;
     const bool hedge = cx.m_strip < 0 || cx.m_strip + Q * kLaneCount > a.cols;
+    cx.hedge = hedge;
     cx.n0 = a.row_begin + r;
     cx.n1 = cx.n0 + seg_len;
     cx.first = max(0, cx.n0 - G::up);
@@ -798,18 +945,21 @@ __global__ void __launch_bounds__(WARPS* kLaneCount)
     // that are not stored; start them at zero so nothing uninitialised is read.
     Pipe pipe{};
 
-    // Steady range: every stage interior, every row loaded and stored.
+    // Steady range: every stage interior, every row loaded and stored.  The
+    // checked ticks before and after it share one code copy (two rounds of
+    // the outer loop); the steady ticks run in their own tight inner loop.
     const int steady_lo = G::down + max(cx.n0, G::kMaxUp);
     const int steady_hi = min(a.rows - 1, cx.n1 - 1 + G::down);
+    int t = cx.first;
+    // first tick of the steady loop: >= steady_lo and a multiple of the period
+    const int s0 = ((max(steady_lo, t) + kP - 1) / kP) * kP;
+    const bool has_steady = s0 + kP - 1 <= steady_hi;
+    const int s1 = has_steady ? s0 + ((steady_hi - s0 + 1) / kP) * kP : s0;  // one past the steady ticks
 #pragma unroll 1
-    for (int t = cx.first; t <= last_tick;) {
-      if (t >= steady_lo && t % kP == 0 && t + kP - 1 <= steady_hi) {
-        if (hedge)
-          steady_chunk<true, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, Phases{});
-        else
-          steady_chunk<false, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, Phases{});
-        t += kP;
-      } else {
+    for (int round = 0; round < 2; ++round) {
+      const int stop = (round == 0 && has_steady) ? s0 : last_tick + 1;
+#pragma unroll 1
+      for (; t < stop; ++t) {
         T row[4][Q];
         if (t <= last_load) {
           src.next(row, a, &tmap0, &tmap1, &tmap2, &tmap3);
@@ -819,14 +969,47 @@ __global__ void __launch_bounds__(WARPS* kLaneCount)
 #pragma unroll
             for (int q = 0; q < Q; ++q) row[c][q] = T(0);
         }
-        if (hedge)
-          checked_tick<kP, true>(pipe, row, t, cx, a, sink, Phases{});
-        else
-          checked_tick<kP, false>(pipe, row, t, cx, a, sink, Phases{});
-        ++t;
+        checked_tick<kP>(pipe, row, t, cx, a, sink, Phases{});
       }
+      if (round == 0 && has_steady) {
+        if (hedge || sink.any_scalar) {
+#pragma unroll 1
+          for (; t < s1; t += kP)
+            steady_chunk<1, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, Phases{});
+        } else {
+          // interior strip: no halo folding, vector stores only
+#pragma unroll 1
+          for (; t < s1; t += kP)
+            steady_chunk<0, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, Phases{});
+        }
+      }
+      if (!has_steady) break;
     }
     src.finish();
+  }
+    if (static_end >= total) break;
+    unsigned long long j = 0;
+    if (lane == 0) j = atomicAdd(a.tail_counter, 1ull);
+    j = __shfl_sync(0xffffffffu, j, 0);
+    f = static_end + static_cast<int64_t>(j) * a.tail_chunk;
+    if (f >= total) break;
+    f_end = min(total, f + static_cast<int64_t>(a.tail_chunk));
+  }
+  if (a.tail_counter != nullptr && lane == 0) {
+    // every warp has drawn its last ticket before it gets here
+    if (atomicAdd(a.tail_counter + 1, 1ull) == static_cast<unsigned long long>(a.n_warps) - 1) {
+      a.tail_counter[0] = 0;
+      a.tail_counter[1] = 0;
+      __threadfence();
+    }
+  }
+  if (a.dbg != nullptr && lane == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    a.dbg[4 * gw + 0] = clock64() - clk0;
+    a.dbg[4 * gw + 1] = dbg_rows;
+    a.dbg[4 * gw + 2] = dbg_edge_rows;
+    a.dbg[4 * gw + 3] = smid;
   }
 }
 
