@@ -126,6 +126,15 @@ unsigned long long* tail_counter_slot() {
   return pool[dev] + 2 * (next[dev]++ % kSlots);
 }
 
+// Lower bound on rows per CTA (B2DWT_MIN_ROWS overrides).
+int min_rows() {
+  static int v = [] {
+    const char* e = std::getenv("B2DWT_MIN_ROWS");
+    return e ? std::atoi(e) : 8;
+  }();
+  return v;
+}
+
 // Work split: [0] share of the rows split statically (1/1024), [1] rows per
 // dynamically claimed tail chunk.  B2DWT_STATIC_FRAC / B2DWT_TAIL_ROWS override.
 int split_param(int which) {
@@ -288,7 +297,7 @@ int run_fused(const b2dwt_plan_s& p, FusedLaunch& r) {
   // Small levels are latency-bound (a tick is a long dependent chain), so
   // spread them over the whole machine; 8 rows keeps the cone re-read <= 50%
   // there and negligible on large levels, which fill the machine anyway.
-  r.min_rows_per_warp = 8;
+  r.min_rows_per_warp = min_rows();
   r.edge_cost8 = edge_cost8();
   r.dbg = g_dbg;
   // dynamic tail: a counter slot from the per-device pool (self-resetting)

@@ -17,24 +17,27 @@
 namespace b2dwt {
 namespace {
 
-constexpr int kQ = 2;
-
 // Launch shape per element type: WARPS per CTA, ring STAGES, RPS quad rows
 // per stage.  f32: 4 x 2 x 1 KB = 8 KB ring per warp (16 warps/SM = 128 KB).
 template <class T>
 struct Shape;
 template <>
 struct Shape<float> {
+#ifndef B2DWT_F32_Q
+#define B2DWT_F32_Q 2
+#endif
 #ifndef B2DWT_F32_STAGES
 #define B2DWT_F32_STAGES 4
 #endif
 #ifndef B2DWT_F32_RPS
 #define B2DWT_F32_RPS 4
 #endif
+  static constexpr int kQ = B2DWT_F32_Q;  // quads per lane
   static constexpr int kWarps = 4, kStages = B2DWT_F32_STAGES, kRps = B2DWT_F32_RPS;
 };
 template <>
 struct Shape<double> {
+  static constexpr int kQ = 2;
   static constexpr int kWarps = 4, kStages = 3, kRps = 2;
 };
 
@@ -95,7 +98,7 @@ template <class Prog, class T, int LIN, int LOUT, bool kStrict, bool kTma>
 cudaError_t launch(const FusedLaunch& r) {
   using S = Shape<T>;
   using Args = StreamArgs<T, (Prog::kNumTerms > 0 ? Prog::kNumTerms : 1)>;
-  constexpr int kWarps = S::kWarps, kStages = S::kStages, kRps = S::kRps;
+  constexpr int kWarps = S::kWarps, kStages = S::kStages, kRps = S::kRps, kQ = S::kQ;
   auto kern = stream_kernel<Prog, T, kQ, LIN, LOUT, kStrict, kTma, kWarps, kStages, kRps>;
   constexpr size_t kRing = static_cast<size_t>(kWarps) * kStages * kRps * RowGeom<T, kQ>::kBytes;
   constexpr size_t kSmem = kRing + (kTma ? kWarps * kStages * sizeof(uint64_t) : 0);
@@ -150,15 +153,19 @@ cudaError_t launch(const FusedLaunch& r) {
   // per-segment cone overhead stays bounded).
   const int64_t kMinRows = std::max(1, r.min_rows_per_warp);
   const int rows_out = r.row_end - r.row_begin;
-  const int64_t resident = static_cast<int64_t>(num_sms()) * blocks_per_sm * kWarps;
-  const int64_t total_rows = static_cast<int64_t>(r.batch) * a.n_strips * rows_out;
-  const int64_t n_warps = std::max<int64_t>(1, std::min(resident, (total_rows + kMinRows - 1) / kMinRows));
-  a.n_warps = static_cast<int>(n_warps);
+  const int64_t resident_ctas = static_cast<int64_t>(num_sms()) * blocks_per_sm;
+  const int64_t n_super = (a.n_strips + kWarps - 1) / kWarps;
+  const int64_t total_rows = static_cast<int64_t>(r.batch) * n_super * rows_out;
+  const int64_t n_ctas = std::max<int64_t>(1, std::min(resident_ctas, (total_rows + kMinRows - 1) / kMinRows));
+  a.n_warps = static_cast<int>(n_ctas);
   a.edge_cost = std::max(8, r.edge_cost8);
   a.dbg = r.dbg;
-  a.tail_counter = r.tail_counter;
+  // Small levels (few rows per CTA) are latency-bound: chunking them only adds
+  // prologues, so the tail shrinks with the per-CTA share and vanishes below it.
+  const int64_t rows_per_cta = total_rows / n_ctas;
+  a.tail_counter = rows_per_cta >= 64 ? r.tail_counter : nullptr;
   a.static_frac = std::min(1024, std::max(0, r.static_frac));
-  a.tail_chunk = std::max(1, r.tail_rows) * 8;
+  a.tail_chunk = static_cast<int>(std::max<int64_t>(4, std::min<int64_t>(r.tail_rows, rows_per_cta / 8))) * 8;
 
   CUtensorMap maps[4];
   memset(maps, 0, sizeof(maps));
@@ -174,7 +181,7 @@ cudaError_t launch(const FusedLaunch& r) {
           return cudaErrorNotSupported;
     }
   }
-  const unsigned grid = static_cast<unsigned>((n_warps + kWarps - 1) / kWarps);
+  const unsigned grid = static_cast<unsigned>(n_ctas);
   kern<<<grid, kWarps * kLaneCount, kSmem, r.stream>>>(a, maps[0], maps[1], maps[2], maps[3]);
   return cudaGetLastError();
 }

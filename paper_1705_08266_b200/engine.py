@@ -420,11 +420,11 @@ class Transform:
             "dwt",
         )
 
-    def capture_dwt(self, x, levels: int):
+    def capture_dwt(self, x, levels: int, level_events: bool = False):
         """Capture the whole ``levels``-deep pyramid of the device image ``x``
         into a CUDA graph (one host submission per pyramid).  Returns a
         :class:`PyramidGraph`; write new pixels into ``x`` and ``replay()``."""
-        return PyramidGraph(self, x, levels)
+        return PyramidGraph(self, x, levels, level_events)
 
     def idwt(self, ll, details, out=None, stream=None):
         torch = self._check(ll, "ll")
@@ -452,25 +452,55 @@ class PyramidGraph:
 
     The graph bakes in the device addresses of ``x`` and of the outputs
     (``ll``, ``details``), which it owns; each :meth:`replay` recomputes the
-    pyramid of whatever ``x`` holds."""
+    pyramid of whatever ``x`` holds.  With ``level_events=True`` an external
+    CUDA event node is recorded before every level and after the last one, so
+    per-level kernel times can be read after a replay (:meth:`level_ms`).
+    """
 
-    def __init__(self, tr: Transform, x, levels: int):
+    def __init__(self, tr: Transform, x, levels: int, level_events: bool = False):
         torch = tr._check(x, "x")
         h, w = x.shape
         self.x = x
+        self.levels = levels
         self.ll, self.details = tr.dwt(x, levels)  # allocates + warms up every level
         self.scratch = torch.empty(((h // 2) * (w // 2) + (h // 4) * (w // 4),), dtype=x.dtype, device=x.device) \
             if levels > 1 else None
-        tr.dwt_into(x, levels, self.details, self.ll, self.scratch)
+        # per-level output views: level l writes LL into scratch (or the final ll)
+        half = (h // 2) * (w // 2)
+        self._ll_views = []
+        for lvl in range(levels):
+            hh_, ww_ = h >> (lvl + 1), w >> (lvl + 1)
+            if lvl == levels - 1:
+                self._ll_views.append(self.ll)
+            else:
+                off = 0 if lvl % 2 == 0 else half
+                self._ll_views.append(self.scratch[off:off + hh_ * ww_].view(hh_, ww_))
+        self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(levels + 1)] \
+            if level_events else None
+        self._run(tr)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            tr.dwt_into(x, levels, self.details, self.ll, self.scratch)
-        self.levels = levels
+            self._run(tr)
+
+    def _run(self, tr):
+        src = self.x
+        for lvl in range(self.levels):
+            if self.events is not None:
+                self.events[lvl].record()
+            hl, lh, hh = self.details[lvl]
+            tr.forward(src, out=(self._ll_views[lvl], hl, lh, hh))
+            src = self._ll_views[lvl]
+        if self.events is not None:
+            self.events[self.levels].record()
 
     def replay(self):
         self.graph.replay()
         return self.ll, self.details
+
+    def level_ms(self):
+        """Kernel time of each level in the last replay (needs level_events=True)."""
+        return [self.events[i].elapsed_time(self.events[i + 1]) for i in range(self.levels)]
 
 
 _TRANSFORMS: dict = {}
