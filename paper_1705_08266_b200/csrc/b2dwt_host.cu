@@ -140,7 +140,7 @@ int min_rows() {
 int split_param(int which) {
   static const int v[3] = {[] {
                              const char* e = std::getenv("B2DWT_STATIC_FRAC");
-                             return e ? std::atoi(e) : 512;
+                             return e ? std::atoi(e) : 768;
                            }(),
                            [] {
                              const char* e = std::getenv("B2DWT_TAIL_ROWS");
@@ -158,7 +158,7 @@ int split_param(int which) {
 int edge_cost8() {
   static int v = [] {
     const char* e = std::getenv("B2DWT_EDGE_COST8");
-    const int x = e ? std::atoi(e) : 12;
+    const int x = e ? std::atoi(e) : 8;
     return x < 8 ? 8 : x;
   }();
   return v;
