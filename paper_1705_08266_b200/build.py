@@ -105,6 +105,13 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
                 ["-std=c++20", *defs, f"-DB2DWT_VID={vid}"] + ([] if real else ["-DB2DWT_STUB"]),
                 os.path.join(BUILD, f"ptxas_{ident}_{vid}{tag}.log"),
             ))
+    # objects built with other experiment flags are stale too
+    flags_file = os.path.join(BUILD, "nvcc_extra.txt")
+    extra = os.environ.get("B2DWT_NVCC_EXTRA", "")
+    if os.path.exists(flags_file) and open(flags_file).read() != extra:
+        force = True
+    with open(flags_file, "w") as fh:
+        fh.write(extra)
     todo = [t for t in tasks if force or _stale(t[1], deps)]
     if verbose:
         print(f"[b2dwt] compiling {len(todo)} units with {jobs} jobs", file=sys.stderr)

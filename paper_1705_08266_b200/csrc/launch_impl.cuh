@@ -32,8 +32,11 @@ struct Shape<float> {
 #ifndef B2DWT_F32_RPS
 #define B2DWT_F32_RPS 4
 #endif
+#ifndef B2DWT_F32_WARPS
+#define B2DWT_F32_WARPS 4
+#endif
   static constexpr int kQ = B2DWT_F32_Q;  // quads per lane
-  static constexpr int kWarps = 4, kStages = B2DWT_F32_STAGES, kRps = B2DWT_F32_RPS;
+  static constexpr int kWarps = B2DWT_F32_WARPS, kStages = B2DWT_F32_STAGES, kRps = B2DWT_F32_RPS;
 };
 template <>
 struct Shape<double> {
