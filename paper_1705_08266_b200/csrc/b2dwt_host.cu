@@ -138,7 +138,7 @@ int min_rows() {
 // Work split: [0] share of the rows split statically (1/1024), [1] rows per
 // dynamically claimed tail chunk.  B2DWT_STATIC_FRAC / B2DWT_TAIL_ROWS override.
 int split_param(int which) {
-  static const int v[3] = {[] {
+  static const int v[5] = {[] {
                              const char* e = std::getenv("B2DWT_STATIC_FRAC");
                              return e ? std::atoi(e) : 768;
                            }(),
@@ -149,6 +149,14 @@ int split_param(int which) {
                            [] {
                              const char* e = std::getenv("B2DWT_STRIP_ALIGN");
                              return e ? std::atoi(e) : 0;
+                           }(),
+                           [] {
+                             const char* e = std::getenv("B2DWT_FULL_ROWS");
+                             return e ? std::atoi(e) : 0;
+                           }(),
+                           [] {
+                             const char* e = std::getenv("B2DWT_PDL");
+                             return e ? std::atoi(e) : 1;
                            }()};
   return v[which];
 }
@@ -305,6 +313,8 @@ int run_fused(const b2dwt_plan_s& p, FusedLaunch& r) {
   r.static_frac = split_param(0);
   r.tail_rows = split_param(1);
   r.strip_align = split_param(2);
+  r.full_rows = split_param(3);
+  r.pdl = split_param(4) != 0;
   bool used_tma = false;
   const cudaError_t e = b.launch(r, &used_tma);
   if (e == cudaErrorNotSupported) return fail(B2DWT_EUNSUPPORTED, "no compiled fused variant for this request");

@@ -36,6 +36,8 @@ struct FusedLaunch {
   int static_frac;        // share of the work split statically (1/1024)
   int tail_rows;          // rows per dynamic tail chunk
   int strip_align;        // strip start / width alignment in quads (>= 2)
+  int full_rows;
+  bool pdl;               // launch with programmatic stream serialization          // rows per CTA needed before a second/third CTA per SM is used (0: always full)
   cudaStream_t stream;
 };
 

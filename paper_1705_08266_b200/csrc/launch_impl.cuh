@@ -126,6 +126,7 @@ cudaError_t launch(const FusedLaunch& r) {
   }
   a.in_bstride = r.in_bstride;
   a.in_row0 = r.in_row0;
+  a.in_row_end = r.in_row0 + r.in_rows;
   a.out_img = static_cast<T*>(r.out_img);
   a.out_bstride = r.out_bstride;
   a.out_row0 = r.out_row0;
@@ -140,6 +141,10 @@ cudaError_t launch(const FusedLaunch& r) {
   // (TMA itself faults below 16 B) and each output row segment is a whole
   // number of 32-B sectors at a sector boundary -- partial sectors written by
   // two strips cost a DRAM read-modify-write (measured: 0.59 -> 0.48 ms at C3).
+  // the kernel addresses output rows with 32-bit byte pitches
+  for (int c = 0; c < (LOUT == kLayoutInterleaved ? 1 : 4); ++c)
+    if (r.out_ld[c] < 0 || r.out_ld[c] * static_cast<int64_t>(sizeof(T)) > int64_t{0x7fffffff})
+      return cudaErrorNotSupported;
   using C = Cone<Prog>;
   constexpr int kInQuadBytes = static_cast<int>(sizeof(T)) * (LIN == kLayoutInterleaved ? 2 : 1);
   constexpr int kOutQuadBytes = static_cast<int>(sizeof(T)) * (LOUT == kLayoutInterleaved ? 2 : 1);
@@ -156,9 +161,12 @@ cudaError_t launch(const FusedLaunch& r) {
   // per-segment cone overhead stays bounded).
   const int64_t kMinRows = std::max(1, r.min_rows_per_warp);
   const int rows_out = r.row_end - r.row_begin;
-  const int64_t resident_ctas = static_cast<int64_t>(num_sms()) * blocks_per_sm;
   const int64_t n_super = (a.n_strips + kWarps - 1) / kWarps;
   const int64_t total_rows = static_cast<int64_t>(r.batch) * n_super * rows_out;
+  int64_t ctas_per_sm = blocks_per_sm;
+  if (r.full_rows > 0)
+    ctas_per_sm = std::max<int64_t>(1, std::min<int64_t>(blocks_per_sm, total_rows / (int64_t{num_sms()} * r.full_rows)));
+  const int64_t resident_ctas = static_cast<int64_t>(num_sms()) * ctas_per_sm;
   const int64_t n_ctas = std::max<int64_t>(1, std::min(resident_ctas, (total_rows + kMinRows - 1) / kMinRows));
   a.n_warps = static_cast<int>(n_ctas);
   a.edge_cost = std::max(8, r.edge_cost8);
@@ -184,9 +192,20 @@ cudaError_t launch(const FusedLaunch& r) {
           return cudaErrorNotSupported;
     }
   }
-  const unsigned grid = static_cast<unsigned>(n_ctas);
-  kern<<<grid, kWarps * kLaneCount, kSmem, r.stream>>>(a, maps[0], maps[1], maps[2], maps[3]);
-  return cudaGetLastError();
+  // Programmatic dependent launch: the kernel's prologue (barriers, descriptor
+  // prefetch, work split) overlaps the tail of the previous kernel on the
+  // stream; it waits (griddepcontrol.wait) before touching global memory.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(n_ctas));
+  cfg.blockDim = dim3(kWarps * kLaneCount);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = r.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = r.pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, maps[0], maps[1], maps[2], maps[3]);
 }
 
 }  // namespace

@@ -54,6 +54,7 @@ struct StreamArgs {
   int64_t in_ld[4];    // elements per image row ([0]) / per plane row
   int64_t in_bstride;  // elements per batch item
   int in_row0;
+  int in_row_end;      // one past the last global quad row the input buffer holds
   // output (buffer row 0 == global quad row out_row0)
   T* out_pl[4];
   T* out_img;
@@ -173,11 +174,11 @@ struct Stage<P, T, Q, kStrict, S, false> {
     constexpr int kSlotIn = cmod(PH - kLag, NW);
     if constexpr (HEDGE == 2) {
       if (cx.hedge)
-        append<true>(in, w[kSlotIn], cx);
+        append<2>(in, w[kSlotIn], cx);
       else
-        append<false>(in, w[kSlotIn], cx);
+        append<0>(in, w[kSlotIn], cx);
     } else {
-      append<HEDGE == 1>(in, w[kSlotIn], cx);
+      append<HEDGE>(in, w[kSlotIn], cx);
     }
     constexpr int kOff = cmod(PH - kLag - D, NW);  // slot of row n
     T out[4][Q];
@@ -210,7 +211,9 @@ struct Stage<P, T, Q, kStrict, S, false> {
   }
 
   // Window row = input row plus left/right halo from the neighbour lanes.
-  template <bool HEDGE>
+  // HEDGE: 0 interior strip, 1 image-edge strip of a wide image (single fold;
+  // the unchecked loop), 2 any image-edge strip (checked ticks only).
+  template <int HEDGE>
   __device__ __forceinline__ static void append(const T (&in)[4][Q], T (&x)[4][E], const Ctx& cx) {
     append_comp<0, HEDGE>(in, x[0], cx);
     append_comp<1, HEDGE>(in, x[1], cx);
@@ -218,7 +221,7 @@ struct Stage<P, T, Q, kStrict, S, false> {
     append_comp<3, HEDGE>(in, x[3], cx);
   }
 
-  template <int C, bool HEDGE>
+  template <int C, int HEDGE>
   __device__ __forceinline__ static void append_comp(const T (&in)[4][Q], T (&x)[E], const Ctx& cx) {
     constexpr CompNeed nd = P::need(S, C);
     if constexpr (nd.used) {
@@ -237,7 +240,7 @@ struct Stage<P, T, Q, kStrict, S, false> {
         // column cols fold their out-of-image slots onto the mirrored in-image
         // slots of the SAME window (single-fold whole-sample symmetry,
         // engine.py:55-92) -- predicated selects, no extra shuffles.
-        if (cx.fold1) {
+        if (HEDGE == 1 || cx.fold1) {
 #pragma unroll
           for (int e = 0; e < L; ++e)
             if (L - e <= nd.left) x[e] = shfl_up1(in[C][Q - L + e]);
@@ -261,7 +264,7 @@ struct Stage<P, T, Q, kStrict, S, false> {
               if (dm >= -L && dm < kk) constexpr_if_fold(x, k == kk, L + d, L + dm);
             }
           }
-        } else {
+        } else if constexpr (HEDGE == 2) {
           // Narrow images: generic gather through the full (periodic) map.
 #pragma unroll
           for (int e = 0; e < E; ++e) {
@@ -366,12 +369,11 @@ template <class P, class T, int Q, bool kStrict, int S>
 struct Stage<P, T, Q, kStrict, S, true> {
   template <int PH, bool CHECK, int HEDGE, class Args, class Sink>
   __device__ __forceinline__ void tick(const T (&in)[4][Q], int t, const Ctx& cx, const Args& a, Sink& sink) {
+    // unchecked segments run whole periods past both ends of their rows: the
+    // row mask is the store predicate
     const int n = t - Geo<P>::down;
-    if constexpr (CHECK) {
-      if (n < cx.n0 || n >= cx.n1) return;
-    }
     // the interior steady path only ever has full, aligned lanes or idle lanes
-    sink.template store<CHECK || HEDGE != 0>(in, n);
+    sink.template store<CHECK || HEDGE != 0>(in, n, n >= cx.n0 && n < cx.n1);
   }
 };
 
@@ -380,11 +382,36 @@ struct Stage<P, T, Q, kStrict, S, true> {
 template <class T, int Q, int LOUT>
 struct StoreSink;
 
-// Four planes, Q consecutive quads per lane.
+// Predicated vector store of one lane's Q values (no branch: the row-range and
+// lane masks become the instruction predicate).
+template <class T, int Q>
+__device__ __forceinline__ void st_pred(char* p, const T (&v)[Q], bool ok) {
+  if constexpr (Q == 2 && sizeof(T) == 4) {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %3, 0;\n@p st.global.v2.f32 [%0], {%1, %2};\n}\n" ::"l"(p),
+                 "f"(v[0]), "f"(v[1]), "r"(static_cast<int>(ok))
+                 : "memory");
+  } else if constexpr (Q == 4 && sizeof(T) == 4) {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %5, 0;\n@p st.global.v4.f32 [%0], {%1, %2, %3, %4};\n}\n" ::"l"(p),
+                 "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "r"(static_cast<int>(ok))
+                 : "memory");
+  } else if constexpr (Q == 2 && sizeof(T) == 8) {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %3, 0;\n@p st.global.v2.f64 [%0], {%1, %2};\n}\n" ::"l"(p),
+                 "d"(v[0]), "d"(v[1]), "r"(static_cast<int>(ok))
+                 : "memory");
+  } else {
+    if (ok) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) reinterpret_cast<T*>(p)[q] = v[q];
+    }
+  }
+}
+
+// Four planes, Q consecutive quads per lane.  Row addresses are byte pointers
+// plus 32-bit byte pitches (one wide multiply-add per plane and row).
 template <class T, int Q>
 struct StoreSink<T, Q, kLayoutPlanar> {
-  T* base[4];      // plane c at row 0 of the global grid, this lane's column
-  int64_t ld[4];
+  char* base[4];   // plane c at row 0 of the global grid, this lane's column
+  int ldb[4];      // row pitch in bytes
   bool full, vec;  // all Q slots stored / vector store legal
   bool any_scalar; // some lane of the warp stores slot by slot
   unsigned mask;   // per-slot store mask when !full
@@ -399,16 +426,18 @@ struct StoreSink<T, Q, kLayoutPlanar> {
     full = mask == (1u << Q) - 1;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      ld[c] = a.out_ld[c];
-      base[c] = a.out_pl[c] + boff - static_cast<int64_t>(a.out_row0) * ld[c] + m_lane;
-      v = v && (ld[c] % Q == 0) && (reinterpret_cast<uintptr_t>(base[c]) % (sizeof(T) * Q) == 0);
+      ldb[c] = static_cast<int>(a.out_ld[c] * static_cast<int64_t>(sizeof(T)));
+      T* p = a.out_pl[c] + boff - static_cast<int64_t>(a.out_row0) * a.out_ld[c] + m_lane;
+      base[c] = reinterpret_cast<char*>(p);
+      v = v && (a.out_ld[c] % Q == 0) && (reinterpret_cast<uintptr_t>(p) % (sizeof(T) * Q) == 0);
     }
     vec = v;
     any_scalar = __any_sync(0xffffffffu, mask != 0 && !(full && vec));
   }
 
+  // Store row n if `in_range` (the caller's row mask).
   template <bool kScalar>
-  __device__ __forceinline__ void store(const T (&v)[4][Q], int n) {
+  __device__ __forceinline__ void store(const T (&v)[4][Q], int n, bool in_range) {
 #ifdef B2DWT_EXPERIMENT_NOSTORE
     // load-path ceiling experiment: keep the values alive, store (almost) nothing
     T acc = T(0);
@@ -416,34 +445,24 @@ struct StoreSink<T, Q, kLayoutPlanar> {
     for (int c = 0; c < 4; ++c)
 #pragma unroll
       for (int q = 0; q < Q; ++q) acc += v[c][q];
-    if (acc == T(-12345)) base[0][n] = acc;
+    if (acc == T(-12345)) reinterpret_cast<T*>(base[0])[n] = acc;
     return;
 #endif
+    const bool vok = in_range && full && vec;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
 #ifdef B2DWT_EXPERIMENT_L2STORE
       // write-path experiment: same instructions, all rows folded into 64 rows (L2 resident)
-      T* p = base[c] + static_cast<int64_t>(n & 63) * ld[c];
+      char* p = base[c] + static_cast<int64_t>(n & 63) * ldb[c];
 #else
-      T* p = base[c] + static_cast<int64_t>(n) * ld[c];
+      char* p = base[c] + static_cast<int64_t>(n) * ldb[c];
 #endif
-      if (full && vec) {
-        if constexpr (Q == 2 && sizeof(T) == 4) {
-          *reinterpret_cast<float2*>(p) = make_float2(v[c][0], v[c][1]);
-        } else if constexpr (Q == 4 && sizeof(T) == 4) {
-          *reinterpret_cast<float4*>(p) = make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
-        } else if constexpr (Q == 2 && sizeof(T) == 8) {
-          *reinterpret_cast<double2*>(p) = make_double2(v[c][0], v[c][1]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < Q; ++q) p[q] = v[c][q];
-        }
-      }
+      st_pred<T, Q>(p, v[c], vok);
       if (kScalar && any_scalar) {  // warp-uniform: only warps that own ragged / unaligned lanes
-        if (!(full && vec)) {
+        if (in_range && !(full && vec)) {
 #pragma unroll
           for (int q = 0; q < Q; ++q)
-            if (mask & (1u << q)) p[q] = v[c][q];
+            if (mask & (1u << q)) reinterpret_cast<T*>(p)[q] = v[c][q];
         }
       }
     }
@@ -453,8 +472,8 @@ struct StoreSink<T, Q, kLayoutPlanar> {
 // Interleaved image: quad (n, m) -> pixels (2n, 2m) .. (2n+1, 2m+1).
 template <class T, int Q>
 struct StoreSink<T, Q, kLayoutInterleaved> {
-  T* base;
-  int64_t ld;
+  char* base;
+  int ldb;  // image row pitch in bytes
   bool full, vec, any_scalar;
   unsigned mask;
 
@@ -465,40 +484,41 @@ struct StoreSink<T, Q, kLayoutInterleaved> {
     for (int q = 0; q < Q; ++q)
       if (m_lane + q >= vlo && m_lane + q < vhi) mask |= 1u << q;
     full = mask == (1u << Q) - 1;
-    ld = a.out_ld[0];
-    base = a.out_img + boff - 2 * static_cast<int64_t>(a.out_row0) * ld + 2 * m_lane;
-    vec = (ld * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0;
+    const int64_t ld = a.out_ld[0];
+    ldb = static_cast<int>(ld * static_cast<int64_t>(sizeof(T)));
+    T* p = a.out_img + boff - 2 * static_cast<int64_t>(a.out_row0) * ld + 2 * m_lane;
+    base = reinterpret_cast<char*>(p);
+    vec = (ld * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(p) % 16) == 0;
     any_scalar = __any_sync(0xffffffffu, mask != 0 && !(full && vec));
   }
 
   template <bool kScalar>
-  __device__ __forceinline__ void store(const T (&v)[4][Q], int n) {
+  __device__ __forceinline__ void store(const T (&v)[4][Q], int n, bool in_range) {
+    const bool vok = in_range && full && vec;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      T* p = base + static_cast<int64_t>(2 * n + h) * ld;
+      char* p = base + static_cast<int64_t>(2 * n + h) * ldb;
       T px[2 * Q];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         px[2 * q] = v[2 * h][q];
         px[2 * q + 1] = v[2 * h + 1][q];
       }
-      if (full && vec) {
+      constexpr int kVec = 16 / static_cast<int>(sizeof(T));
 #pragma unroll
-        for (int i = 0; i < 2 * Q; i += 16 / static_cast<int>(sizeof(T))) {
-          if constexpr (sizeof(T) == 4) {
-            *reinterpret_cast<float4*>(p + i) = make_float4(px[i], px[i + 1], px[i + 2], px[i + 3]);
-          } else {
-            *reinterpret_cast<double2*>(p + i) = make_double2(px[i], px[i + 1]);
-          }
-        }
+      for (int i = 0; i < 2 * Q; i += kVec) {
+        T chunk[kVec];
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) chunk[e] = px[i + e];
+        st_pred<T, kVec>(p + i * sizeof(T), chunk, vok);
       }
       if (kScalar && any_scalar) {
-        if (!(full && vec)) {
+        if (in_range && !(full && vec)) {
 #pragma unroll
           for (int q = 0; q < Q; ++q)
             if (mask & (1u << q)) {
-              p[2 * q] = px[2 * q];
-              p[2 * q + 1] = px[2 * q + 1];
+              reinterpret_cast<T*>(p)[2 * q] = px[2 * q];
+              reinterpret_cast<T*>(p)[2 * q + 1] = px[2 * q + 1];
             }
         }
       }
@@ -678,12 +698,19 @@ __device__ __forceinline__ void fill_row_cpasync(T* stage, int j, int gr, int64_
 }
 
 // Streams quad rows first .. last_load of one (strip, segment) through the ring.
+// Ring stages cover global rows [k*RPS, (k+1)*RPS): the first stage starts at
+// the multiple of RPS at or below `first` (TMA zero-fills rows outside the
+// buffer; cp.async skips rows before `first`), so stage switches fall on the
+// same global rows in every segment and an unrolled tick loop whose period
+// divides RPS meets them only at its first tick.
 template <class T, int Q, int LIN, bool kTma, int STAGES, int RPS>
 struct RowSource {
   static constexpr int kStageElems = RPS * RowGeom<T, Q>::kElems;
+  static constexpr int kStageRows = RPS;
   T* ring;
   uint64_t* bars;
   int first, last_load, n_stages;
+  int row0;   // global row of the segment's first ring stage (multiple of RPS)
   int k, j;   // current stage within the segment, row within the stage
   int base;   // stages consumed by earlier segments (mbarrier phase continuity)
   const T* slot;
@@ -702,7 +729,7 @@ struct RowSource {
       if (lane == 0) {
         uint64_t* bar = bars + (g % STAGES);
         mbar_expect_tx(bar, kStageElems * sizeof(T));
-        const int r0 = first + kk * RPS - a.in_row0;
+        const int r0 = row0 + kk * RPS - a.in_row0;
         if constexpr (LIN == kLayoutInterleaved) {
           tma_load_3d(s, tm0, bar, 2 * m_strip, 2 * r0, b);
         } else {
@@ -717,8 +744,8 @@ struct RowSource {
       if (kk < n_stages) {
 #pragma unroll 1
         for (int jj = 0; jj < RPS; ++jj) {
-          const int gr = first + kk * RPS + jj;
-          if (gr <= last_load) fill_row_cpasync<T, Q, LIN, RPS>(s, jj, gr, boff, lane, m_lane, cols, a);
+          const int gr = row0 + kk * RPS + jj;
+          if (gr >= first && gr <= last_load) fill_row_cpasync<T, Q, LIN, RPS>(s, jj, gr, boff, lane, m_lane, cols, a);
         }
       }
       cp_async_commit();
@@ -744,11 +771,35 @@ struct RowSource {
     }
   }
 
+  // Switch to the next ring stage: wait for it, refill the slot freed by the
+  // previous one.
+  template <class Args>
+  __device__ __forceinline__ void advance(const Args& a, const CUtensorMap* tm0, const CUtensorMap* tm1,
+                                          const CUtensorMap* tm2, const CUtensorMap* tm3) {
+    ++k;
+    const int g = base + k;
+    if constexpr (kTma) {
+#ifndef B2DWT_EXPERIMENT_NOLOAD
+      mbar_wait(bars + (g % STAGES), (g / STAGES) & 1);
+#endif
+      __syncwarp();
+      if (k + STAGES - 1 < n_stages) {
+        if (lane == 0) fence_proxy_async();
+        issue(k + STAGES - 1, a, tm0, tm1, tm2, tm3);
+      }
+    } else {
+      cp_async_wait<STAGES - 2>();
+      issue(k + STAGES - 1, a, tm0, tm1, tm2, tm3);
+    }
+    slot = ring + (g % STAGES) * kStageElems;
+  }
+
   // Begin a segment: rows first .. last_load will be consumed in order.
   template <class Args>
   __device__ __forceinline__ void start(const Args& a, const CUtensorMap* tm0, const CUtensorMap* tm1,
                                         const CUtensorMap* tm2, const CUtensorMap* tm3) {
-    n_stages = (last_load - first + RPS) / RPS;
+    row0 = first - first % RPS;
+    n_stages = (last_load - row0 + RPS) / RPS;
     if constexpr (kTma) {
       __syncwarp();  // every lane is done reading the previous segment's slots
       if (lane == 0) fence_proxy_async();
@@ -757,7 +808,8 @@ struct RowSource {
       for (int kk = 0; kk < STAGES - 1; ++kk) issue(kk, a, tm0, tm1, tm2, tm3);
     }
     k = -1;
-    j = RPS - 1;
+    advance(a, tm0, tm1, tm2, tm3);
+    j = first - row0 - 1;
   }
 
   // End a segment (all its stages were consumed).
@@ -772,24 +824,24 @@ struct RowSource {
                                        const CUtensorMap* tm1, const CUtensorMap* tm2, const CUtensorMap* tm3) {
     if (++j == RPS) {
       j = 0;
-      ++k;
-      const int g = base + k;
-      if constexpr (kTma) {
-#ifndef B2DWT_EXPERIMENT_NOLOAD
-        mbar_wait(bars + (g % STAGES), (g / STAGES) & 1);
-#endif
-        __syncwarp();
-        // slot (g-1) % STAGES was consumed in the previous round: refill it
-        if (k + STAGES - 1 < n_stages) {
-          if (lane == 0) fence_proxy_async();
-          issue(k + STAGES - 1, a, tm0, tm1, tm2, tm3);
-        }
-      } else {
-        cp_async_wait<STAGES - 2>();
-        issue(k + STAGES - 1, a, tm0, tm1, tm2, tm3);
-      }
-      slot = ring + (g % STAGES) * kStageElems;
+      advance(a, tm0, tm1, tm2, tm3);
     }
+    read_row<T, Q, LIN, RPS>(slot, j, lane, row);
+  }
+
+  // Split form for loops whose period divides RPS: one stage check per
+  // period (at a global row that is a multiple of the period), then rows
+  // without checks.
+  template <class Args>
+  __device__ __forceinline__ void advance_if_due(const Args& a, const CUtensorMap* tm0, const CUtensorMap* tm1,
+                                                 const CUtensorMap* tm2, const CUtensorMap* tm3) {
+    if (j == RPS - 1) {
+      j = -1;
+      advance(a, tm0, tm1, tm2, tm3);
+    }
+  }
+  __device__ __forceinline__ void next_row(T (&row)[4][Q]) {
+    ++j;
     read_row<T, Q, LIN, RPS>(slot, j, lane, row);
   }
 };
@@ -817,7 +869,12 @@ __device__ __forceinline__ void steady_chunk(Pipe& pipe, Src& src, int t, const 
                                              const CUtensorMap* m3, std::integer_sequence<int, I...>) {
   T row[sizeof...(I)][4][Q];
   // One row at a time: load, then push through every stage.
-  ((src.next(row[I], a, m0, m1, m2, m3), run_tick<I, false, HEDGE>(pipe, row[I], t + I, cx, a, sink)), ...);
+  if constexpr (Src::kStageRows % static_cast<int>(sizeof...(I)) == 0) {
+    src.advance_if_due(a, m0, m1, m2, m3);  // t is a multiple of the period: the only possible stage switch
+    ((src.next_row(row[I]), run_tick<I, false, HEDGE>(pipe, row[I], t + I, cx, a, sink)), ...);
+  } else {
+    ((src.next(row[I], a, m0, m1, m2, m3), run_tick<I, false, HEDGE>(pipe, row[I], t + I, cx, a, sink)), ...);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -889,6 +946,10 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
   src.lane = lane;
   src.cols = a.cols;
   src.init_barriers(&tmap0, &tmap1, &tmap2, &tmap3);
+  // PDL: let the next kernel on the stream start its own prologue, then wait
+  // for the previous one (our input) to complete before any global access.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
 #pragma unroll 1
   for (;;) {
@@ -937,8 +998,19 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
     const int last_load = min(a.rows - 1, cx.n1 - 1 + G::down);
     const int last_tick = cx.n1 - 1 + G::down;
 
-    src.first = cx.first;
-    src.last_load = last_load;
+    // Vertically interior segment: every row the stored rows depend on lies
+    // inside the image and the input buffer, so no stage ever reflects a row.
+    // Run it entirely in the unchecked loop over whole periods: the extra fill
+    // ticks before n0 compute rows outside the stored rows' cone (never read
+    // by them), and the sink masks rows outside [n0, n1).
+    const int t_lo = (cx.first / kP) * kP;
+    const int t_hi = ((last_tick + kP) / kP) * kP;  // one past the last tick
+    // (edge strips of narrow images need the generic column map: checked ticks only)
+    const bool steady_ok = !hedge || cx.fold1;
+    const bool unchecked = steady_ok && cx.n0 - G::up >= 0 && last_tick < a.rows && t_lo >= a.in_row0 &&
+                           t_hi <= a.in_row_end;
+    src.first = unchecked ? t_lo : cx.first;
+    src.last_load = unchecked ? t_hi - 1 : last_load;
     src.m_lane = cx.m_lane;
     src.m_strip = cx.m_strip;
     src.b = b;
@@ -958,14 +1030,15 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
     // the outer loop); the steady ticks run in their own tight inner loop.
     const int steady_lo = G::down + max(cx.n0, G::kMaxUp);
     const int steady_hi = min(a.rows - 1, cx.n1 - 1 + G::down);
-    int t = cx.first;
+    int t = unchecked ? t_lo : cx.first;
     // first tick of the steady loop: >= steady_lo and a multiple of the period
-    const int s0 = ((max(steady_lo, t) + kP - 1) / kP) * kP;
-    const bool has_steady = s0 + kP - 1 <= steady_hi;
-    const int s1 = has_steady ? s0 + ((steady_hi - s0 + 1) / kP) * kP : s0;  // one past the steady ticks
+    const int s0 = unchecked ? t_lo : ((max(steady_lo, t) + kP - 1) / kP) * kP;
+    const bool has_steady = unchecked || (steady_ok && s0 + kP - 1 <= steady_hi);
+    const int s1 = unchecked ? t_hi : has_steady ? s0 + ((steady_hi - s0 + 1) / kP) * kP : s0;  // one past the steady ticks
+    const int t_end = unchecked ? t_hi : last_tick + 1;
 #pragma unroll 1
     for (int round = 0; round < 2; ++round) {
-      const int stop = (round == 0 && has_steady) ? s0 : last_tick + 1;
+      const int stop = (round == 0 && has_steady) ? s0 : t_end;
 #pragma unroll 1
       for (; t < stop; ++t) {
         T row[4][Q];
