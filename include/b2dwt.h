@@ -62,7 +62,9 @@ enum {
                                 rounded separately, in compiled term order (default) */
     B2DWT_FAST = 2,          /* fused multiply-add; within 1e-4 x input range (f32)  */
     B2DWT_FORCE_GENERIC = 4, /* use the per-sub-step interpreter kernel (debug)      */
-    B2DWT_NO_TMA = 8         /* fused kernel loads with cp.async instead of TMA      */
+    B2DWT_NO_TMA = 8,        /* fused kernel loads with cp.async instead of TMA      */
+    B2DWT_NO_TILE = 16,      /* never use the 2-D tile kernel (small levels stream)  */
+    B2DWT_FORCE_TILE = 32    /* tile kernel for every whole-image level it supports  */
 };
 
 /* One multiply-accumulate term: out[target][n,m] += coeff * in[src][n+dn, m+dm] */
@@ -150,6 +152,23 @@ int b2dwt_dwt(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t heig
  * `scratch` as for b2dwt_dwt. */
 int b2dwt_idwt(b2dwt_plan plan, const void* ll, int64_t ll_ld, const b2dwt_planes* details, int32_t levels,
                void* image, int64_t image_ld, int64_t height, int64_t width, void* scratch, void* stream);
+
+/* Multi-level forward pyramid of a HOST image into HOST subbands (the
+ * reference's host-array call, engine.py:481-487, iterated on LL), with the
+ * PCIe traffic pipelined: the image is uploaded in `bands` row chunks on one
+ * internal stream, every level is computed band by band (b2dwt_forward_rows)
+ * on `stream` as soon as its input rows plus the cone exist, and each finished
+ * band's HL/LH/HH rows (and the final LL) are downloaded on a second internal
+ * stream while later bands are still uploading.  `details[l].ptr[1..3]` and
+ * `ll_out` are host pointers (pinned memory gives the overlap; pageable memory
+ * is correct but serialises the copies).  `workspace` is device memory of at
+ * least b2dwt_dwt_host_workspace() bytes, 256-B aligned.  Asynchronous: the
+ * outputs are complete once `stream` reaches the point of the call.  Needs a
+ * fused built-in forward plan; bit-identical to b2dwt_dwt.  bands <= 0: 16. */
+int64_t b2dwt_dwt_host_workspace(b2dwt_plan plan, int64_t height, int64_t width, int32_t levels);
+int b2dwt_dwt_host(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t height, int64_t width,
+                   int32_t levels, const b2dwt_planes* details, void* ll_out, int64_t ll_ld, void* workspace,
+                   int64_t workspace_bytes, int32_t bands, void* stream);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ B2DWT_EINVAL = -22
 B2DWT_EUNSUPPORTED = -95
 B2DWT_ECUDA = -5
 F32, F64 = 0, 1
-STRICT, FAST, FORCE_GENERIC, NO_TMA = 1, 2, 4, 8
+STRICT, FAST, FORCE_GENERIC, NO_TMA, NO_TILE, FORCE_TILE = 1, 2, 4, 8, 16, 32
 
 # Every symbol include/b2dwt.h declares (tests check the .so exports all of them).
 EXPORTS = (
@@ -35,6 +35,8 @@ EXPORTS = (
     "b2dwt_forward_rows",
     "b2dwt_dwt",
     "b2dwt_idwt",
+    "b2dwt_dwt_host_workspace",
+    "b2dwt_dwt_host",
 )
 
 
@@ -120,6 +122,8 @@ def load():
             "b2dwt_forward_rows": (ctypes.c_int, [vp, vp, i64, i64, i64, i64, i64, i64, i64, P(Planes), vp]),
             "b2dwt_dwt": (ctypes.c_int, [vp, vp, i64, i64, i64, i32, P(Planes), vp, i64, vp, vp]),
             "b2dwt_idwt": (ctypes.c_int, [vp, vp, i64, P(Planes), i32, vp, i64, i64, i64, vp, vp]),
+            "b2dwt_dwt_host_workspace": (i64, [vp, i64, i64, i32]),
+            "b2dwt_dwt_host": (ctypes.c_int, [vp, vp, i64, i64, i64, i32, P(Planes), vp, i64, vp, i64, i32, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -2,9 +2,11 @@
 
 Translation units:
   csrc/b2dwt_host.cu        C ABI, plan matching, generic interpreter kernel
+  csrc/host_pipeline.cu     b2dwt_dwt_host: host-buffer pyramid, copies overlapped in row bands
   csrc/prog_dispatch.cu     per built-in program: variant selection, cone
   csrc/prog_variant.cu      ONE fused kernel per unit (program x element type x
                             layout x arithmetic x fill), compiled in parallel
+  csrc/prog_tile.cu         per built-in program: the small-level tile kernels
 
 Flags: -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 (ptxas -v output is
 kept in build/ptxas_<unit>.log for register / spill review).
@@ -52,10 +54,24 @@ def _program_units():
     return units
 
 
-def _deps():
-    return [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".inc", ".cu"))] + [
-        os.path.join(INCLUDE, "b2dwt.h")
-    ]
+def _deps(src: str, seen=None):
+    """The source and every file it includes with #include "..." (recursively)."""
+    seen = set() if seen is None else seen
+    src = os.path.normpath(src)
+    if src in seen or not os.path.exists(src):
+        return seen
+    seen.add(src)
+    with open(src) as fh:
+        for line in fh:
+            line = line.strip()
+            if line.startswith("#include") and '"' in line:
+                name = line.split('"')[1]
+                for base in (os.path.dirname(src), CSRC, INCLUDE):
+                    cand = os.path.join(base, name)
+                    if os.path.exists(cand):
+                        _deps(cand, seen)
+                        break
+    return seen
 
 
 def _stale(target: str, deps) -> bool:
@@ -79,12 +95,11 @@ def _compile(args):
 
 def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    deps = _deps()
     jobs = jobs or max(1, os.cpu_count() or 1)
     # host TU in C++17 (nvcc 12.9's C++20 front end trips over libstdc++ 13
     # containers); kernel TUs need C++20 for the phase-unrolled tick loop
-    tasks = [(os.path.join(CSRC, "b2dwt_host.cu"), os.path.join(BUILD, "b2dwt_host.o"), ["-std=c++17"],
-              os.path.join(BUILD, "ptxas_b2dwt_host.log"))]
+    tasks = [(os.path.join(CSRC, f"{u}.cu"), os.path.join(BUILD, f"{u}.o"), ["-std=c++17"],
+              os.path.join(BUILD, f"ptxas_{u}.log")) for u in ("b2dwt_host", "host_pipeline")]
     # dev builds: B2DWT_PROGRAMS=ident,... and/or B2DWT_VARIANTS=0,1 compile
     # only that subset; the rest are stubs (the host falls back to the generic
     # interpreter for them).  Release builds compile everything.
@@ -96,6 +111,10 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
         defs = [f"-DB2DWT_PROG={ident}", f"-DB2DWT_PROG_INV={int(inv)}"]
         tasks.append((os.path.join(CSRC, "prog_dispatch.cu"), os.path.join(BUILD, f"dispatch_{ident}.o"),
                       ["-std=c++20", *defs], os.path.join(BUILD, f"ptxas_dispatch_{ident}.log")))
+        tag = "" if (only is None or ident in only) else "_stub"
+        tasks.append((os.path.join(CSRC, "prog_tile.cu"), os.path.join(BUILD, f"tile_{ident}{tag}.o"),
+                      ["-std=c++20", *defs] + (["-DB2DWT_STUB"] if tag else []),
+                      os.path.join(BUILD, f"ptxas_tile_{ident}{tag}.log")))
         for vid in range(N_VARIANTS):
             real = (only is None or ident in only) and (vonly is None or vid in vonly)
             tag = "" if real else "_stub"
@@ -112,7 +131,14 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
         force = True
     with open(flags_file, "w") as fh:
         fh.write(extra)
-    todo = [t for t in tasks if force or _stale(t[1], deps)]
+    dep_cache = {}
+
+    def unit_deps(src):
+        if src not in dep_cache:
+            dep_cache[src] = sorted(_deps(src))
+        return dep_cache[src]
+
+    todo = [t for t in tasks if force or _stale(t[1], unit_deps(t[0]))]
     if verbose:
         print(f"[b2dwt] compiling {len(todo)} units with {jobs} jobs", file=sys.stderr)
     todo.sort(key=lambda t: ("_stub" in t[1] or "dispatch_" in t[1], t[1]))

@@ -25,6 +25,7 @@ namespace b2dwt {
 
 #define B2DWT_DECLARE(ID, NAME)                                     \
   cudaError_t b2dwt_fused_##NAME(const FusedLaunch&, bool* used_tma); \
+  cudaError_t b2dwt_tile_##NAME(const FusedLaunch&);                  \
   ConeInfo b2dwt_cone_##NAME();
 B2DWT_FOR_EACH_PROGRAM(B2DWT_DECLARE)
 #undef B2DWT_DECLARE
@@ -52,6 +53,7 @@ struct Builtin {
   TermInfo (*term)(int);
   double (*coef)(int);
   FusedLauncher launch;
+  TileLauncher tile;
   ConeGetter cone;
   bool inverse;
 };
@@ -73,7 +75,7 @@ const Builtin* builtins() {
   static const Builtin table[] = {
 #define B2DWT_ROW(ID, NAME)                                                                                      \
   {progs::NAME::kKey,        progs::NAME::kNumSub, progs::NAME::kNumTerms, &begin_of<progs::NAME>,             \
-   &term_of<progs::NAME>,    &coef_of<progs::NAME>,    &b2dwt_fused_##NAME,  &b2dwt_cone_##NAME,     std::strstr(progs::NAME::kKey, "/inv") \
+   &term_of<progs::NAME>,    &coef_of<progs::NAME>,    &b2dwt_fused_##NAME,  &b2dwt_tile_##NAME, &b2dwt_cone_##NAME,     std::strstr(progs::NAME::kKey, "/inv") \
    != nullptr},
       B2DWT_FOR_EACH_PROGRAM(B2DWT_ROW)
 #undef B2DWT_ROW
@@ -82,6 +84,10 @@ const Builtin* builtins() {
 }
 
 }  // namespace
+
+// Error reporting for the other host units (host_pipeline.cu).
+int set_last_error(int code, const char* msg) { return fail(code, msg); }
+
 }  // namespace b2dwt
 
 using namespace b2dwt;
@@ -159,6 +165,24 @@ int split_param(int which) {
                              return e ? std::atoi(e) : 1;
                            }()};
   return v[which];
+}
+
+// Largest level (batch x quads) served by the tile kernel; B2DWT_TILE_MAX_QUADS overrides.
+int64_t tile_max_quads() {
+  static int64_t v = [] {
+    const char* e = std::getenv("B2DWT_TILE_MAX_QUADS");
+    return e ? std::atoll(e) : int64_t{1} << 18;  // measured: levels <= 512^2 quads
+  }();
+  return v;
+}
+
+// Tile window rows (16 or 32); 0 = the launcher decides.  B2DWT_TILE_ROWS overrides.
+int tile_rows_for() {
+  static int forced = [] {
+    const char* e = std::getenv("B2DWT_TILE_ROWS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return forced;
 }
 
 // Relative cost of an image-edge strip row (eighths of an interior row) used to
@@ -315,6 +339,22 @@ int run_fused(const b2dwt_plan_s& p, FusedLaunch& r) {
   r.strip_align = split_param(2);
   r.full_rows = split_param(3);
   r.pdl = split_param(4) != 0;
+  // Small whole-image levels run the 2-D tile kernel: the streaming kernel's
+  // per-warp row pipelines are too short there to hide their latency.
+  const int64_t quads = static_cast<int64_t>(r.batch) * r.rows * r.cols;
+  const bool whole = r.row_begin == 0 && r.row_end == r.rows && r.in_row0 == 0 && r.out_row0 == 0 &&
+                     r.in_rows == r.rows;
+  const bool tile_ok = (p.flags & B2DWT_NO_TILE) == 0 &&
+                       (quads <= tile_max_quads() || (p.flags & B2DWT_FORCE_TILE) != 0);
+  if (whole && tile_ok) {
+    r.use_tile = true;
+    r.tile_rows = tile_rows_for();
+    const cudaError_t e = b.tile(r);
+    if (e == cudaSuccess) return B2DWT_OK;
+    if (e != cudaErrorNotSupported) return cuda_fail(e, "fused tile kernel");
+    (void)cudaGetLastError();
+    r.use_tile = false;
+  }
   bool used_tma = false;
   const cudaError_t e = b.launch(r, &used_tma);
   if (e == cudaErrorNotSupported) return fail(B2DWT_EUNSUPPORTED, "no compiled fused variant for this request");

@@ -1,0 +1,235 @@
+// host_pipeline.cu -- b2dwt_dwt_host: the multi-level forward pyramid of a
+// HOST image into HOST subbands, with the PCIe copies overlapped against each
+// other and against the kernels.
+//
+// The reference's public call (liftfuse forward(), engine.py:481-487) takes
+// and returns host arrays.  Done naively on a GPU that is upload -> pyramid ->
+// download, three serial phases, and for a 16384^2 f32 image the two copies
+// (1 GiB each way) are ~98% of the time.  Host-to-device and device-to-host
+// copies use different copy engines and PCIe directions, so they can run at
+// the same time if the work is cut into row bands:
+//
+//   s_in  : H2D of image row chunk 0, 1, ..., K-1 (one event per chunk)
+//   s_comp: level-l band k (b2dwt_forward_rows) as soon as its input rows plus
+//           the program's cone exist -- H2D chunks for level 0, bands of
+//           level l-1 for level l (a wavefront down the pyramid)
+//   s_out : D2H of each finished band's HL/LH/HH rows (and the final LL)
+//
+// so the download of level 0 runs under the upload, and only the last band's
+// work is exposed.  Every level keeps its own LL buffer in the workspace (all
+// levels are in flight at once, so the ping-pong of b2dwt_dwt cannot be used).
+// Results are bit-identical to b2dwt_dwt: row bands reproduce the whole-image
+// transform exactly (b2dwt_forward_rows).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/b2dwt.h"
+
+namespace b2dwt {
+int set_last_error(int code, const char* msg);  // b2dwt_host.cu: b2dwt_last_error() text
+}
+
+namespace {
+
+constexpr size_t kAlign = 256;
+
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Layout {
+  size_t image = 0;               // device copy of the input image
+  std::vector<size_t> ll;         // LL output of level l (input of level l+1; last = final LL)
+  std::vector<size_t> det;        // HL/LH/HH of level l, three planes back to back
+  size_t total = 0;
+};
+
+Layout layout_of(int64_t h, int64_t w, int levels, size_t es) {
+  Layout L;
+  size_t off = 0;
+  L.image = off;
+  off = align_up(off + static_cast<size_t>(h * w) * es);
+  for (int l = 0; l < levels; ++l) {
+    const size_t q = static_cast<size_t>((h >> (l + 1)) * (w >> (l + 1))) * es;
+    L.ll.push_back(off);
+    off = align_up(off + q);
+    L.det.push_back(off);
+    off = align_up(off + 3 * align_up(q));
+  }
+  L.total = off;
+  return L;
+}
+
+// Quad-row range [b0, b1) of band k of K over R rows.
+void band_rows(int64_t R, int K, int k, int64_t* b0, int64_t* b1) {
+  *b0 = R * k / K;
+  *b1 = R * (k + 1) / K;
+}
+
+struct Resources {
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> events;
+  ~Resources() {
+    for (cudaEvent_t e : events) cudaEventDestroy(e);  // released once the GPU is past them
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+  }
+  cudaError_t event(cudaEvent_t* e) {
+    const cudaError_t r = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+    if (r == cudaSuccess) events.push_back(*e);
+    return r;
+  }
+};
+
+int pipe_fail(int code, const std::string& msg) { return b2dwt::set_last_error(code, msg.c_str()); }
+
+}  // namespace
+
+extern "C" {
+
+int64_t b2dwt_dwt_host_workspace(b2dwt_plan plan, int64_t height, int64_t width, int32_t levels) {
+  b2dwt_plan_info info;
+  if (b2dwt_plan_get_info(plan, &info) != B2DWT_OK || levels < 1 || height < 2 || width < 2) return -1;
+  return static_cast<int64_t>(layout_of(height, width, levels, info.dtype == B2DWT_F32 ? 4 : 8).total);
+}
+
+int b2dwt_dwt_host(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t height, int64_t width,
+                   int32_t levels, const b2dwt_planes* details, void* ll_out, int64_t ll_ld, void* workspace,
+                   int64_t workspace_bytes, int32_t bands, void* stream) {
+  b2dwt_plan_info info;
+  if (int rc = b2dwt_plan_get_info(plan, &info)) return rc;
+  if (levels < 1) return pipe_fail(B2DWT_EINVAL, "levels must be >= 1");
+  if (!image || !details || !ll_out || !workspace) return pipe_fail(B2DWT_EINVAL, "null pointer");
+  if (height < 2 || width < 2 || (height % (2LL << (levels - 1))) || (width % (2LL << (levels - 1))))
+    return pipe_fail(B2DWT_EINVAL, "height and width must be divisible by 2^levels");
+  if (image_ld < width || ll_ld < (width >> levels)) return pipe_fail(B2DWT_EINVAL, "row pitch smaller than width");
+  if (info.kernel != 1 || std::strstr(info.key, "/fwd") == nullptr)
+    return pipe_fail(B2DWT_EUNSUPPORTED, "host pipeline needs a fused built-in forward program");
+  const size_t es = info.dtype == B2DWT_F32 ? 4 : 8;
+  const Layout L = layout_of(height, width, levels, es);
+  if (workspace_bytes < static_cast<int64_t>(L.total)) return pipe_fail(B2DWT_EINVAL, "workspace too small");
+  if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return pipe_fail(B2DWT_EINVAL, "workspace must be 256-B aligned");
+  char* ws = static_cast<char*>(workspace);
+  cudaStream_t s_comp = static_cast<cudaStream_t>(stream);
+  // bands per level: at least one, at most what keeps every band >= the cone
+  const int64_t cone = std::max<int64_t>(1, std::max(info.halo_up, info.halo_down));
+  int K = bands > 0 ? bands : 16;
+  const int64_t R_last = height >> levels;  // quad rows of the coarsest level
+  K = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(K, R_last / cone)));
+
+  Resources res;
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&res.s_in, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&res.s_out, cudaStreamNonBlocking)) != cudaSuccess)
+    return pipe_fail(B2DWT_ECUDA, std::string("stream create: ") + cudaGetErrorString(e));
+  cudaEvent_t ev_start;
+  if ((e = res.event(&ev_start)) != cudaSuccess || (e = cudaEventRecord(ev_start, s_comp)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(res.s_in, ev_start, 0)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(res.s_out, ev_start, 0)) != cudaSuccess)
+    return pipe_fail(B2DWT_ECUDA, std::string("event: ") + cudaGetErrorString(e));
+
+  // 1. upload in K row chunks (even pixel rows), all enqueued up front so every
+  //    event exists before a compute band waits on it
+  char* dimg = ws + L.image;
+  std::vector<cudaEvent_t> ev_in(K);
+  std::vector<int64_t> chunk_end(K);  // pixel rows uploaded after chunk c
+  for (int c = 0; c < K; ++c) {
+    const int64_t p0 = 2 * (height / 2 * c / K), p1 = 2 * (height / 2 * (c + 1) / K);
+    chunk_end[c] = p1;
+    if (p1 > p0) {
+      e = cudaMemcpy2DAsync(dimg + static_cast<size_t>(p0 * width) * es, width * es,
+                            static_cast<const char*>(image) + static_cast<size_t>(p0 * image_ld) * es, image_ld * es,
+                            width * es, p1 - p0, cudaMemcpyHostToDevice, res.s_in);
+      if (e != cudaSuccess) return pipe_fail(B2DWT_ECUDA, std::string("H2D: ") + cudaGetErrorString(e));
+    }
+    if ((e = res.event(&ev_in[c])) != cudaSuccess || (e = cudaEventRecord(ev_in[c], res.s_in)) != cudaSuccess)
+      return pipe_fail(B2DWT_ECUDA, std::string("event: ") + cudaGetErrorString(e));
+  }
+
+  // 2. wavefront of bands; 3. downloads behind each band
+  std::vector<std::vector<cudaEvent_t>> ev_band(levels, std::vector<cudaEvent_t>(K));
+  std::vector<int> next(levels, 0);
+  auto input_ready_band = [&](int l, int k) -> int {
+    // index of the producer (H2D chunk for l == 0, band of level l-1) that
+    // completes the input rows band (l, k) needs, cone included
+    const int64_t R = height >> (l + 1);  // quad rows of level l
+    int64_t b0, b1;
+    band_rows(R, K, k, &b0, &b1);
+    const int64_t need_px = 2 * std::min<int64_t>(R, b1 + info.halo_down);  // pixel rows of level-l input
+    if (l == 0) {
+      int c = 0;
+      while (c < K - 1 && chunk_end[c] < need_px) ++c;
+      return c;
+    }
+    const int64_t Rp = height >> l;  // quad rows of level l-1 = pixel rows of level-l input
+    int kp = 0;
+    int64_t p0, p1;
+    for (;; ++kp) {
+      band_rows(Rp, K, kp, &p0, &p1);
+      if (p1 >= need_px || kp == K - 1) break;
+    }
+    return kp;
+  };
+  int remaining = levels * K;
+  while (remaining > 0) {
+    bool progressed = false;
+    for (int l = 0; l < levels; ++l) {
+      while (next[l] < K) {
+        const int k = next[l];
+        const int dep = input_ready_band(l, k);
+        if (l > 0 && dep >= next[l - 1]) break;  // producer not enqueued yet
+        cudaEvent_t wait = l == 0 ? ev_in[dep] : ev_band[l - 1][dep];
+        if ((e = cudaStreamWaitEvent(s_comp, wait, 0)) != cudaSuccess)
+          return pipe_fail(B2DWT_ECUDA, std::string("wait: ") + cudaGetErrorString(e));
+        const int64_t h = height >> l, w = width >> l, R = h / 2, C = w / 2;
+        int64_t b0, b1;
+        band_rows(R, K, k, &b0, &b1);
+        if (b1 > b0) {
+          const char* in = l == 0 ? dimg : ws + L.ll[l - 1];
+          char* det = ws + L.det[l];
+          const size_t plane = align_up(static_cast<size_t>(R * C) * es);
+          b2dwt_planes out;
+          out.ptr[0] = ws + L.ll[l] + static_cast<size_t>(b0 * C) * es;
+          for (int c = 1; c < 4; ++c) out.ptr[c] = det + (c - 1) * plane + static_cast<size_t>(b0 * C) * es;
+          for (int c = 0; c < 4; ++c) out.ld[c] = C;
+          out.bstride = 0;
+          if (int rc = b2dwt_forward_rows(plan, in, w, 0, h, h, w, b0, b1, &out, s_comp)) return rc;
+        }
+        if ((e = res.event(&ev_band[l][k])) != cudaSuccess || (e = cudaEventRecord(ev_band[l][k], s_comp)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(res.s_out, ev_band[l][k], 0)) != cudaSuccess)
+          return pipe_fail(B2DWT_ECUDA, std::string("event: ") + cudaGetErrorString(e));
+        if (b1 > b0) {
+          const size_t plane = align_up(static_cast<size_t>(R * C) * es);
+          for (int c = 1; c < 4; ++c) {
+            const char* src = ws + L.det[l] + (c - 1) * plane + static_cast<size_t>(b0 * C) * es;
+            char* dst = static_cast<char*>(details[l].ptr[c]) + static_cast<size_t>(b0 * details[l].ld[c]) * es;
+            e = cudaMemcpy2DAsync(dst, details[l].ld[c] * es, src, C * es, C * es, b1 - b0, cudaMemcpyDeviceToHost,
+                                  res.s_out);
+            if (e != cudaSuccess) return pipe_fail(B2DWT_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
+          }
+          if (l == levels - 1) {
+            const char* src = ws + L.ll[l] + static_cast<size_t>(b0 * C) * es;
+            char* dst = static_cast<char*>(ll_out) + static_cast<size_t>(b0 * ll_ld) * es;
+            e = cudaMemcpy2DAsync(dst, ll_ld * es, src, C * es, C * es, b1 - b0, cudaMemcpyDeviceToHost, res.s_out);
+            if (e != cudaSuccess) return pipe_fail(B2DWT_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
+          }
+        }
+        ++next[l];
+        --remaining;
+        progressed = true;
+      }
+    }
+    if (!progressed) return pipe_fail(B2DWT_EINVAL, "internal: band schedule stalled");
+  }
+  // the caller's stream sees everything complete after this point
+  cudaEvent_t ev_done;
+  if ((e = res.event(&ev_done)) != cudaSuccess || (e = cudaEventRecord(ev_done, res.s_out)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(s_comp, ev_done, 0)) != cudaSuccess)
+    return pipe_fail(B2DWT_ECUDA, std::string("event: ") + cudaGetErrorString(e));
+  return B2DWT_OK;
+}
+
+}  // extern "C"

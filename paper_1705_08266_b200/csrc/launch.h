@@ -37,7 +37,9 @@ struct FusedLaunch {
   int tail_rows;          // rows per dynamic tail chunk
   int strip_align;        // strip start / width alignment in quads (>= 2)
   int full_rows;
-  bool pdl;               // launch with programmatic stream serialization          // rows per CTA needed before a second/third CTA per SM is used (0: always full)
+  bool pdl;               // launch with programmatic stream serialization
+  bool use_tile;          // run the 2-D tile kernel (tile_kernel.cuh) instead
+  int tile_rows;          // its window rows (16 / 32), 0 = by level size
   cudaStream_t stream;
 };
 
@@ -48,6 +50,7 @@ struct ConeInfo {
 
 // Returns cudaSuccess or the launch error; `used_tma` reports the fill path.
 using FusedLauncher = cudaError_t (*)(const FusedLaunch&, bool* used_tma);
+using TileLauncher = cudaError_t (*)(const FusedLaunch&);
 using ConeGetter = ConeInfo (*)();
 
 }  // namespace b2dwt

@@ -276,7 +276,7 @@ class Transform:
     """
 
     def __init__(self, scheme, precision: str = "single", fast: bool = False, tma: bool = True,
-                 force_generic: bool = False):
+                 force_generic: bool = False, tile: bool | None = None):
         self.scheme = scheme
         self.precision = precision
         self.np_dtype = np.dtype(PRECISION_DTYPES[precision])
@@ -286,6 +286,8 @@ class Transform:
             flags |= _native.NO_TMA
         if force_generic:
             flags |= _native.FORCE_GENERIC
+        if tile is not None:  # None: small levels tile, large ones stream
+            flags |= _native.FORCE_TILE if tile else _native.NO_TILE
         self.flags = flags
         self.fwd_program, self.inv_program = _programs(scheme)
         self.fwd_plan = plan_for(self.fwd_program, self.dtype, flags)
@@ -419,6 +421,58 @@ class Transform:
                                      _stream_handle(torch, stream)),
             "dwt",
         )
+
+    def dwt_host(self, x, levels: int, details=None, ll=None, bands: int = 16, stream=None, sync: bool = True):
+        """Pyramid of a HOST image into HOST subbands (b2dwt_dwt_host).
+
+        ``x`` is a CPU tensor or NumPy array ``[H, W]``.  The upload, the
+        band-by-band kernels and the downloads are pipelined (pinned host
+        memory gives the copy overlap; pageable memory still works).  Outputs
+        default to new pinned CPU tensors; pass ``details`` /  ``ll`` to reuse
+        them.  Returns ``(ll, details)``; with ``sync=False`` they are valid
+        once ``stream`` (default: current) has reached this point.
+        """
+        torch = _require_cuda()
+        if isinstance(x, np.ndarray):
+            x = torch.from_numpy(np.ascontiguousarray(x))
+        if x.device.type != "cpu":
+            raise ValueError("dwt_host takes a host (CPU) image; use dwt() for device tensors")
+        if x.dim() != 2 or x.stride(1) != 1:
+            raise ValueError("dwt_host takes one [H, W] image with contiguous rows")
+        if x.dtype != self.torch_dtype:
+            raise TypeError(f"expected {self.torch_dtype}, got {x.dtype}")
+        h, w = x.shape
+        if levels < 1:
+            raise ValueError("levels must be >= 1")
+        if h % (1 << levels) or w % (1 << levels):
+            raise ValueError(f"dimensions must be divisible by 2^{levels}, got {w}x{h}")
+        pin = x.is_pinned()
+        if details is None:
+            details = [tuple(torch.empty((h >> (l + 1), w >> (l + 1)), dtype=x.dtype, pin_memory=pin)
+                             for _ in range(3)) for l in range(levels)]
+        if ll is None:
+            ll = torch.empty((h >> levels, w >> levels), dtype=x.dtype, pin_memory=pin)
+        lib = _native.load()
+        need = int(lib.b2dwt_dwt_host_workspace(self.fwd_plan.handle, h, w, levels))
+        if need < 0:
+            raise ValueError("bad dwt_host geometry")
+        ws = getattr(self, "_host_ws", None)
+        if ws is None or ws.numel() < need:
+            ws = torch.empty((need,), dtype=torch.uint8, device="cuda")
+            self._host_ws = ws
+        arr = (_native.Planes * levels)()
+        for lvl, (hl, lh, hh) in enumerate(details):
+            arr[lvl] = _native.planes([0, _ptr(hl), _ptr(lh), _ptr(hh)],
+                                      [0, hl.stride(0), lh.stride(0), hh.stride(0)], 0)
+        s = _stream_handle(torch, stream)
+        _native.check(
+            lib.b2dwt_dwt_host(self.fwd_plan.handle, _ptr(x), x.stride(0), h, w, levels, arr, _ptr(ll),
+                               ll.stride(0), _ptr(ws), ws.numel(), bands, s),
+            "dwt_host",
+        )
+        if sync:
+            (stream if stream is not None else torch.cuda.current_stream()).synchronize()
+        return ll, details
 
     def capture_dwt(self, x, levels: int, level_events: bool = False):
         """Capture the whole ``levels``-deep pyramid of the device image ``x``
@@ -583,8 +637,17 @@ def dwt(image: Image2D, scheme, levels: int = 1, cfg: TileConfig | None = None) 
     _check_tile(cfg, compile_scheme(scheme))
     torch = _require_cuda()
     tr = _transform(scheme, image.precision)
-    ll, details = tr.dwt(_to_device(torch, image.data), levels)
+    a = image.data
+    if tr.fwd_plan.fused and a.size >= _HOST_PIPELINE_MIN_PX and a.shape[0] % (1 << levels) == 0 \
+            and a.shape[1] % (1 << levels) == 0:
+        # large host image: uploads, kernels and downloads overlapped in row bands
+        ll, details = tr.dwt_host(a, levels)
+        return Pyramid(Image2D(ll.numpy()), tuple(tuple(Image2D(b.numpy()) for b in d) for d in details))
+    ll, details = tr.dwt(_to_device(torch, a), levels)
     return Pyramid(Image2D(_to_host(ll)), tuple(tuple(Image2D(_to_host(b)) for b in d) for d in details))
+
+
+_HOST_PIPELINE_MIN_PX = 1 << 22  # below ~4 Mpx the copies are too short to pipeline
 
 
 def idwt(pyramid: Pyramid, scheme, cfg: TileConfig | None = None) -> Image2D:

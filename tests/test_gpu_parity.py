@@ -41,6 +41,8 @@ def _transform_from_programs(fwd_prog, inv_prog, precision, **kw):
         flags |= _native.NO_TMA
     if kw.get("force_generic"):
         flags |= _native.FORCE_GENERIC
+    if kw.get("tile") is not None:
+        flags |= _native.FORCE_TILE if kw["tile"] else _native.NO_TILE
     t.flags = flags
     t.fwd_program, t.inv_program = fwd_prog, inv_prog
     t.fwd_plan = plan_for(fwd_prog, t.dtype, flags)
@@ -61,10 +63,10 @@ def _host(t):
     return t.cpu().numpy()
 
 
-VARIANTS = [dict(), dict(tma=False), dict(force_generic=True)]
+VARIANTS = [dict(tile=False), dict(tile=False, tma=False), dict(tile=True), dict(force_generic=True)]
 
 
-@pytest.mark.parametrize("variant", VARIANTS, ids=["fused-tma", "fused-cpasync", "generic"])
+@pytest.mark.parametrize("variant", VARIANTS, ids=["stream-tma", "stream-cpasync", "tile", "generic"])
 def test_vectors_bit_exact(variant):
     vec = G.vectors()
     checked = 0
@@ -99,7 +101,7 @@ def test_fused_kernel_selected_for_cdf_programs():
     assert not _golden_transform("haar-like", "non-separable-split", "single").fwd_plan.fused
 
 
-@pytest.mark.parametrize("variant", VARIANTS[:2], ids=["fused-tma", "fused-cpasync"])
+@pytest.mark.parametrize("variant", VARIANTS[:3], ids=["stream-tma", "stream-cpasync", "tile"])
 def test_hashes_bit_exact(variant):
     checked = 0
     for k, digest in G.hashes().items():
@@ -132,14 +134,16 @@ def test_run_components_matches_oracle():
                 assert np.array_equal(_host(g), w), key
 
 
+@pytest.mark.parametrize("tile", [False, True], ids=["stream", "tile"])
 @pytest.mark.parametrize("shape", [(4096, 4096), (2050, 3074), (520, 8200)])
-def test_large_strict_bit_exact_vs_oracle(shape):
-    """Full-size strict parity at C2 size and ragged shapes (multi-strip, multi-segment)."""
+def test_large_strict_bit_exact_vs_oracle(shape, tile):
+    """Full-size strict parity at C2 size and ragged shapes (multi-strip,
+    multi-segment; multi-tile with partial edge tiles for the tile kernel)."""
     progs = G.programs()
     h, w = shape
     img = np.random.default_rng(11).random((h, w)).astype(np.float32)
     for scheme in ("non-separable-split", "separable-convolution"):
-        tr = _golden_transform("cdf97", scheme, "single")
+        tr = _golden_transform("cdf97", scheme, "single", tile=tile)
         got = [_host(c) for c in tr.forward(_dev(img))]
         want = oracle.forward(img, progs[f"cdf97/{scheme}/fwd"])
         for g, wv, n in zip(got, want, NAMES):
@@ -149,21 +153,23 @@ def test_large_strict_bit_exact_vs_oracle(shape):
         assert np.array_equal(rec, want_rec), (scheme, shape)
 
 
-def test_fast_mode_within_north_star_tolerance():
+@pytest.mark.parametrize("tile", [False, True], ids=["stream", "tile"])
+def test_fast_mode_within_north_star_tolerance(tile):
     progs = G.programs()
     img = np.random.default_rng(3).random((1030, 2050)).astype(np.float32)
     rng_ = float(img.max() - img.min())
     for wavelet in ("cdf53", "cdf97"):
         for scheme in ("separable-convolution", "separable-lifting", "non-separable-lifting", "non-separable-split"):
-            tr = _golden_transform(wavelet, scheme, "single", fast=True)
+            tr = _golden_transform(wavelet, scheme, "single", fast=True, tile=tile)
             got = [_host(c) for c in tr.forward(_dev(img))]
             want = oracle.forward(img.astype(np.float64), progs[f"{wavelet}/{scheme}/fwd"])
             err = max(float(np.abs(g - wv).max()) for g, wv in zip(got, want))
             assert err <= 1e-4 * rng_, (wavelet, scheme, err)
 
 
-def test_batch_equals_loop():
-    tr = _golden_transform("cdf97", "non-separable-split", "single")
+@pytest.mark.parametrize("tile", [False, True], ids=["stream", "tile"])
+def test_batch_equals_loop(tile):
+    tr = _golden_transform("cdf97", "non-separable-split", "single", tile=tile)
     x = torch.rand((3, 130, 262), device="cuda")
     batched = tr.forward(x)
     for b in range(3):
@@ -236,3 +242,48 @@ def test_errors_match_reference_messages():
         forward(Image2D(np.zeros((5, 8))), build_scheme("separable-lifting", CDF53))
     with pytest.raises(ValueError, match="smaller than the scheme halo"):
         forward(Image2D.random(32, 32, seed=0), build_scheme("separable-convolution", CDF97), TileConfig(tile=(1, 1)))
+
+
+@pytest.mark.parametrize("shape,levels,bands,pinned", [
+    ((1024, 768), 3, 16, True),
+    ((512, 1024), 5, 7, False),
+    ((2048, 2048), 4, 32, True),
+    ((96, 64), 2, 16, True),  # bands capped by the cone on the coarsest level
+])
+def test_dwt_host_pipeline_equals_device_pyramid(shape, levels, bands, pinned):
+    """b2dwt_dwt_host (banded upload / wavefront / download) is bit-identical to
+    the device pyramid and hence to the iterated reference."""
+    for wavelet in ("cdf53", "cdf97"):
+        tr = _golden_transform(wavelet, "non-separable-split", "single")
+        h, w = shape
+        host = torch.rand((h, w), generator=torch.Generator().manual_seed(h + w))
+        if pinned:
+            host = host.pin_memory()
+        ll_d, det_d = tr.dwt(host.cuda(), levels)
+        ll_h, det_h = tr.dwt_host(host, levels, bands=bands)
+        assert ll_h.device.type == "cpu"
+        assert torch.equal(ll_h, ll_d.cpu()), (wavelet, shape)
+        for lvl in range(levels):
+            for a, b in zip(det_h[lvl], det_d[lvl]):
+                assert torch.equal(a, b.cpu()), (wavelet, shape, lvl)
+
+
+def test_dwt_host_matches_golden_pyramids():
+    pyr = G.pyramids()
+    bases = sorted({k.rsplit("/", 1)[0] if k.endswith(("/ll", "/rec")) else k.rsplit("/", 2)[0] for k in pyr})
+    checked = 0
+    for base in bases:
+        wavelet, scheme, dims, seed, lv, precision = base.split("/")
+        w, h = (int(x) for x in dims.split("x"))
+        levels = int(lv[1:])
+        img = G.random_image(w, h, int(seed[1:]), precision)
+        tr = _golden_transform(wavelet, scheme, precision)
+        if not tr.fwd_plan.fused:
+            continue
+        ll, details = tr.dwt_host(img, levels, bands=4)
+        assert np.array_equal(ll.numpy(), pyr[f"{base}/ll"]), base
+        for lvl, bands in enumerate(details):
+            for name, band in zip(("hl", "lh", "hh"), bands):
+                assert np.array_equal(band.numpy(), pyr[f"{base}/{lvl}/{name}"]), (base, lvl, name)
+        checked += 1
+    assert checked > 0

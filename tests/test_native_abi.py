@@ -93,3 +93,33 @@ def test_no_cpu_fallback_without_device(lib):
     pl = _native.planes([8, 8, 8, 8], [4, 4, 4, 4])
     rc = lib.b2dwt_forward(p.handle, ctypes.c_void_p(16), 8, 0, 8, 8, ctypes.byref(pl), 1, None)
     assert rc == _native.B2DWT_ECUDA
+
+
+def test_dwt_host_workspace_and_validation(lib):
+    """b2dwt_dwt_host: workspace sizing and argument checks are host logic."""
+    p = _native.Plan(compile_scheme(build_scheme("non-separable-split", CDF97)), _native.F32)
+    n, levels = 16384, 5
+
+    def up(x):
+        return (x + 255) // 256 * 256
+
+    want = up(n * n * 4)
+    for lvl in range(levels):
+        q = (n >> (lvl + 1)) ** 2 * 4
+        want = up(want + q)
+        want = up(want + 3 * up(q))
+    assert lib.b2dwt_dwt_host_workspace(p.handle, n, n, levels) == want
+    assert lib.b2dwt_dwt_host_workspace(p.handle, n, n, 0) == -1
+    det = (_native.Planes * levels)()
+    args = (ctypes.c_void_p(4096), n, n, n, levels, det, ctypes.c_void_p(4096), n >> levels)
+    assert lib.b2dwt_dwt_host(p.handle, *args, None, want, 16, None) == _native.B2DWT_EINVAL
+    assert lib.b2dwt_dwt_host(p.handle, *args, ctypes.c_void_p(4096), want - 1, 16, None) == _native.B2DWT_EINVAL
+    assert "workspace too small" in lib.b2dwt_last_error().decode()
+    bad = (ctypes.c_void_p(4096), n, n + 2, n, levels, det, ctypes.c_void_p(4096), n >> levels)
+    assert lib.b2dwt_dwt_host(p.handle, *bad, ctypes.c_void_p(4096), want, 16, None) == _native.B2DWT_EINVAL
+    inv = _native.Plan(compile_scheme(invert_scheme(build_scheme("non-separable-split", CDF97))), _native.F32)
+    assert lib.b2dwt_dwt_host(inv.handle, *args, ctypes.c_void_p(4096), want, 16, None) == \
+        _native.B2DWT_EUNSUPPORTED
+    if lib.b2dwt_device_count() == 0:
+        # valid request, no device: fails loudly, never computes on the CPU
+        assert lib.b2dwt_dwt_host(p.handle, *args, ctypes.c_void_p(4096), want, 16, None) == _native.B2DWT_ECUDA
