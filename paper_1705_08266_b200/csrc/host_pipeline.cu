@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -63,22 +64,17 @@ Layout layout_of(int64_t h, int64_t w, int levels, size_t es) {
   return L;
 }
 
-// Quad-row range [b0, b1) of band k of K over R rows.
-void band_rows(int64_t R, int K, int k, int64_t* b0, int64_t* b1) {
-  *b0 = R * k / K;
-  *b1 = R * (k + 1) / K;
-}
-
 struct Resources {
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> events;
+  bool timing = false;  // B2DWT_PIPE_TRACE: timed events, timeline printed after the call
   ~Resources() {
     for (cudaEvent_t e : events) cudaEventDestroy(e);  // released once the GPU is past them
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
   }
   cudaError_t event(cudaEvent_t* e) {
-    const cudaError_t r = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+    const cudaError_t r = cudaEventCreateWithFlags(e, timing ? cudaEventDefault : cudaEventDisableTiming);
     if (r == cudaSuccess) events.push_back(*e);
     return r;
   }
@@ -114,13 +110,20 @@ int b2dwt_dwt_host(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t
   if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return pipe_fail(B2DWT_EINVAL, "workspace must be 256-B aligned");
   char* ws = static_cast<char*>(workspace);
   cudaStream_t s_comp = static_cast<cudaStream_t>(stream);
-  // bands per level: at least one, at most what keeps every band >= the cone
+  // K row chunks for the upload and level 0; level l uses K >> l bands (at
+  // least one, never thinner than the cone) so the small levels are not cut
+  // into copies too small to run at PCIe speed
   const int64_t cone = std::max<int64_t>(1, std::max(info.halo_up, info.halo_down));
-  int K = bands > 0 ? bands : 16;
-  const int64_t R_last = height >> levels;  // quad rows of the coarsest level
-  K = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(K, R_last / cone)));
+  const int K = std::max(1, bands > 0 ? bands : 16);
+  std::vector<int> KL(levels);
+  for (int l = 0; l < levels; ++l) {
+    const int64_t R = height >> (l + 1);
+    KL[l] = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(std::max(1, K >> l), R / cone)));
+  }
 
   Resources res;
+  res.timing = std::getenv("B2DWT_PIPE_TRACE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> trace;  // (label, event) for the timeline
   cudaError_t e;
   if ((e = cudaStreamCreateWithFlags(&res.s_in, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&res.s_out, cudaStreamNonBlocking)) != cudaSuccess)
@@ -147,88 +150,108 @@ int b2dwt_dwt_host(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t
     }
     if ((e = res.event(&ev_in[c])) != cudaSuccess || (e = cudaEventRecord(ev_in[c], res.s_in)) != cudaSuccess)
       return pipe_fail(B2DWT_ECUDA, std::string("event: ") + cudaGetErrorString(e));
+    if (res.timing) trace.emplace_back("in" + std::to_string(c), ev_in[c]);
   }
 
   // 2. wavefront of bands; 3. downloads behind each band
-  std::vector<std::vector<cudaEvent_t>> ev_band(levels, std::vector<cudaEvent_t>(K));
-  std::vector<int> next(levels, 0);
-  auto input_ready_band = [&](int l, int k) -> int {
-    // index of the producer (H2D chunk for l == 0, band of level l-1) that
-    // completes the input rows band (l, k) needs, cone included
-    const int64_t R = height >> (l + 1);  // quad rows of level l
-    int64_t b0, b1;
-    band_rows(R, K, k, &b0, &b1);
-    const int64_t need_px = 2 * std::min<int64_t>(R, b1 + info.halo_down);  // pixel rows of level-l input
-    if (l == 0) {
-      int c = 0;
-      while (c < K - 1 && chunk_end[c] < need_px) ++c;
-      return c;
+  std::vector<std::vector<cudaEvent_t>> ev_band(levels);
+  for (int l = 0; l < levels; ++l) ev_band[l].resize(KL[l]);
+  // Band boundaries: each band ends `halo_down` quad rows short of what its
+  // producer (H2D chunk / band of the level above) completes, so a band needs
+  // exactly one producer and runs the moment that producer lands.  Level l's
+  // input pixel rows are level l-1's output quad rows.
+  std::vector<std::vector<int64_t>> ends(levels);  // exclusive quad-row ends
+  std::vector<std::vector<int>> deps(levels);      // producer index of each band
+  for (int l = 0; l < levels; ++l) {
+    const int64_t R = height >> (l + 1);
+    const int nprod = l == 0 ? K : KL[l - 1];
+    int64_t prev = 0;
+    for (int k = 0; k < KL[l]; ++k) {
+      const int j = static_cast<int>((static_cast<int64_t>(k) + 1) * nprod / KL[l]) - 1;
+      const int64_t pend = l == 0 ? chunk_end[j] : ends[l - 1][j];  // pixel rows of level-l input
+      int64_t end = k == KL[l] - 1 ? R : std::min<int64_t>(R, pend / 2 - info.halo_down);
+      end = std::max(end, prev);
+      ends[l].push_back(end);
+      deps[l].push_back(j);
+      prev = end;
     }
-    const int64_t Rp = height >> l;  // quad rows of level l-1 = pixel rows of level-l input
-    int kp = 0;
-    int64_t p0, p1;
-    for (;; ++kp) {
-      band_rows(Rp, K, kp, &p0, &p1);
-      if (p1 >= need_px || kp == K - 1) break;
+  }
+  // emission order = execution order on the compute stream: after each
+  // level-0 band, every band of a coarser level whose producer is enqueued
+  auto emit = [&](int l, int k) -> int {
+    cudaStream_t s_o = res.s_out;
+    cudaEvent_t wait = l == 0 ? ev_in[deps[l][k]] : ev_band[l - 1][deps[l][k]];
+    if ((e = cudaStreamWaitEvent(s_comp, wait, 0)) != cudaSuccess)
+      return pipe_fail(B2DWT_ECUDA, std::string("wait: ") + cudaGetErrorString(e));
+    const int64_t h = height >> l, w = width >> l, R = h / 2, C = w / 2;
+    const int64_t b0 = k == 0 ? 0 : ends[l][k - 1], b1 = ends[l][k];
+    if (b1 > b0) {
+      const char* in = l == 0 ? dimg : ws + L.ll[l - 1];
+      char* det = ws + L.det[l];
+      const size_t plane = align_up(static_cast<size_t>(R * C) * es);
+      b2dwt_planes out;
+      out.ptr[0] = ws + L.ll[l] + static_cast<size_t>(b0 * C) * es;
+      for (int c = 1; c < 4; ++c) out.ptr[c] = det + (c - 1) * plane + static_cast<size_t>(b0 * C) * es;
+      for (int c = 0; c < 4; ++c) out.ld[c] = C;
+      out.bstride = 0;
+      if (int rc = b2dwt_forward_rows(plan, in, w, 0, h, h, w, b0, b1, &out, s_comp)) return rc;
     }
-    return kp;
-  };
-  int remaining = levels * K;
-  while (remaining > 0) {
-    bool progressed = false;
-    for (int l = 0; l < levels; ++l) {
-      while (next[l] < K) {
-        const int k = next[l];
-        const int dep = input_ready_band(l, k);
-        if (l > 0 && dep >= next[l - 1]) break;  // producer not enqueued yet
-        cudaEvent_t wait = l == 0 ? ev_in[dep] : ev_band[l - 1][dep];
-        if ((e = cudaStreamWaitEvent(s_comp, wait, 0)) != cudaSuccess)
-          return pipe_fail(B2DWT_ECUDA, std::string("wait: ") + cudaGetErrorString(e));
-        const int64_t h = height >> l, w = width >> l, R = h / 2, C = w / 2;
-        int64_t b0, b1;
-        band_rows(R, K, k, &b0, &b1);
-        if (b1 > b0) {
-          const char* in = l == 0 ? dimg : ws + L.ll[l - 1];
-          char* det = ws + L.det[l];
-          const size_t plane = align_up(static_cast<size_t>(R * C) * es);
-          b2dwt_planes out;
-          out.ptr[0] = ws + L.ll[l] + static_cast<size_t>(b0 * C) * es;
-          for (int c = 1; c < 4; ++c) out.ptr[c] = det + (c - 1) * plane + static_cast<size_t>(b0 * C) * es;
-          for (int c = 0; c < 4; ++c) out.ld[c] = C;
-          out.bstride = 0;
-          if (int rc = b2dwt_forward_rows(plan, in, w, 0, h, h, w, b0, b1, &out, s_comp)) return rc;
-        }
-        if ((e = res.event(&ev_band[l][k])) != cudaSuccess || (e = cudaEventRecord(ev_band[l][k], s_comp)) != cudaSuccess ||
-            (e = cudaStreamWaitEvent(res.s_out, ev_band[l][k], 0)) != cudaSuccess)
-          return pipe_fail(B2DWT_ECUDA, std::string("event: ") + cudaGetErrorString(e));
-        if (b1 > b0) {
-          const size_t plane = align_up(static_cast<size_t>(R * C) * es);
-          for (int c = 1; c < 4; ++c) {
-            const char* src = ws + L.det[l] + (c - 1) * plane + static_cast<size_t>(b0 * C) * es;
-            char* dst = static_cast<char*>(details[l].ptr[c]) + static_cast<size_t>(b0 * details[l].ld[c]) * es;
-            e = cudaMemcpy2DAsync(dst, details[l].ld[c] * es, src, C * es, C * es, b1 - b0, cudaMemcpyDeviceToHost,
-                                  res.s_out);
-            if (e != cudaSuccess) return pipe_fail(B2DWT_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
-          }
-          if (l == levels - 1) {
-            const char* src = ws + L.ll[l] + static_cast<size_t>(b0 * C) * es;
-            char* dst = static_cast<char*>(ll_out) + static_cast<size_t>(b0 * ll_ld) * es;
-            e = cudaMemcpy2DAsync(dst, ll_ld * es, src, C * es, C * es, b1 - b0, cudaMemcpyDeviceToHost, res.s_out);
-            if (e != cudaSuccess) return pipe_fail(B2DWT_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
-          }
-        }
-        ++next[l];
-        --remaining;
-        progressed = true;
+    if ((e = res.event(&ev_band[l][k])) != cudaSuccess || (e = cudaEventRecord(ev_band[l][k], s_comp)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s_o, ev_band[l][k], 0)) != cudaSuccess)
+      return pipe_fail(B2DWT_ECUDA, std::string("event: ") + cudaGetErrorString(e));
+    if (b1 > b0) {
+      const size_t plane = align_up(static_cast<size_t>(R * C) * es);
+      for (int c = 1; c < 4; ++c) {
+        const char* src = ws + L.det[l] + (c - 1) * plane + static_cast<size_t>(b0 * C) * es;
+        char* dst = static_cast<char*>(details[l].ptr[c]) + static_cast<size_t>(b0 * details[l].ld[c]) * es;
+        e = cudaMemcpy2DAsync(dst, details[l].ld[c] * es, src, C * es, C * es, b1 - b0, cudaMemcpyDeviceToHost,
+                              s_o);
+        if (e != cudaSuccess) return pipe_fail(B2DWT_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
+      }
+      if (l == levels - 1) {
+        const char* src = ws + L.ll[l] + static_cast<size_t>(b0 * C) * es;
+        char* dst = static_cast<char*>(ll_out) + static_cast<size_t>(b0 * ll_ld) * es;
+        e = cudaMemcpy2DAsync(dst, ll_ld * es, src, C * es, C * es, b1 - b0, cudaMemcpyDeviceToHost, s_o);
+        if (e != cudaSuccess) return pipe_fail(B2DWT_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
       }
     }
-    if (!progressed) return pipe_fail(B2DWT_EINVAL, "internal: band schedule stalled");
+    if (res.timing) {
+      cudaEvent_t ev_o;
+      if (res.event(&ev_o) == cudaSuccess && cudaEventRecord(ev_o, s_o) == cudaSuccess) {
+        trace.emplace_back("c" + std::to_string(l) + "." + std::to_string(k), ev_band[l][k]);
+        trace.emplace_back("o" + std::to_string(l) + "." + std::to_string(k), ev_o);
+      }
+    }
+    return B2DWT_OK;
+  };
+  std::vector<int> next(levels, 0);
+  for (int k0 = 0; k0 < KL[0]; ++k0) {
+    if (int rc = emit(0, k0)) return rc;
+    next[0] = k0 + 1;
+    for (int l = 1; l < levels; ++l)
+      while (next[l] < KL[l] && deps[l][next[l]] < next[l - 1]) {
+        if (int rc = emit(l, next[l])) return rc;
+        ++next[l];
+      }
   }
   // the caller's stream sees everything complete after this point
   cudaEvent_t ev_done;
   if ((e = res.event(&ev_done)) != cudaSuccess || (e = cudaEventRecord(ev_done, res.s_out)) != cudaSuccess ||
       (e = cudaStreamWaitEvent(s_comp, ev_done, 0)) != cudaSuccess)
     return pipe_fail(B2DWT_ECUDA, std::string("event: ") + cudaGetErrorString(e));
+  if (res.timing && cudaEventSynchronize(ev_done) == cudaSuccess) {
+    std::string line = "[b2dwt pipe] ms:";
+    for (auto& t : trace) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev_start, t.second);
+      char buf[48];
+      std::snprintf(buf, sizeof(buf), " %s=%.2f", t.first.c_str(), ms);
+      line += buf;
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev_start, ev_done);
+    std::fprintf(stderr, "%s done=%.2f\n", line.c_str(), ms);
+  }
   return B2DWT_OK;
 }
 
