@@ -10,6 +10,7 @@
 // reference either way.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -174,6 +175,13 @@ int64_t tile_max_quads() {
     return e ? std::atoll(e) : int64_t{1} << 18;  // measured: levels <= 512^2 quads
   }();
   return v;
+}
+
+// Input bytes per stream-kernel launch before a request is split (0: never);
+// B2DWT_MAX_LAUNCH_BYTES overrides.
+int64_t max_launch_bytes() {
+  const char* e = std::getenv("B2DWT_MAX_LAUNCH_BYTES");  // read per call: tests vary it
+  return e ? std::atoll(e) : int64_t{512} << 20;
 }
 
 // Tile window rows (16 or 32); 0 = the launcher decides.  B2DWT_TILE_ROWS overrides.
@@ -355,8 +363,49 @@ int run_fused(const b2dwt_plan_s& p, FusedLaunch& r) {
     (void)cudaGetLastError();
     r.use_tile = false;
   }
+  // Footprint-bounded launches: one launch spreads its CTAs over the whole
+  // request (each takes a contiguous share of the rows), and past ~1 GiB the
+  // concurrently touched pages outgrow the GPU's translation reach (measured
+  // on 65536^2: 0.70 of copy bandwidth as one launch, 0.82 as 16 row bands).
+  // Large requests therefore run as a sequence of launches of at most
+  // max_launch_bytes of input each: batch chunks, or row bands of one image.
+  const size_t es = r.dtype == 1 ? 8 : 4;
+  const int64_t in_bytes = quads * 4 * static_cast<int64_t>(es);
+  const int64_t cap = max_launch_bytes();
+  int64_t parts = cap > 0 ? (in_bytes + cap - 1) / cap : 1;
+  if (r.batch > 1) parts = std::min<int64_t>(parts, r.batch);
+  else parts = std::min<int64_t>(parts, std::max(1, (r.row_end - r.row_begin) / 256));
   bool used_tma = false;
-  const cudaError_t e = b.launch(r, &used_tma);
+  cudaError_t e = cudaSuccess;
+  if (parts <= 1) {
+    e = b.launch(r, &used_tma);
+  } else if (r.batch > 1) {
+    const int batch = r.batch;
+    for (int64_t i = 0; i < parts && e == cudaSuccess; ++i) {
+      const int i0 = static_cast<int>(batch * i / parts), i1 = static_cast<int>(batch * (i + 1) / parts);
+      FusedLaunch q = r;
+      const int64_t ib = static_cast<int64_t>(i0) * r.in_bstride * static_cast<int64_t>(es);
+      const int64_t ob = static_cast<int64_t>(i0) * r.out_bstride * static_cast<int64_t>(es);
+      if (q.in_img) q.in_img = static_cast<const char*>(q.in_img) + ib;
+      if (q.out_img) q.out_img = static_cast<char*>(q.out_img) + ob;
+      for (int c = 0; c < 4; ++c) {
+        if (q.in_pl[c]) q.in_pl[c] = static_cast<const char*>(q.in_pl[c]) + ib;
+        if (q.out_pl[c]) q.out_pl[c] = static_cast<char*>(q.out_pl[c]) + ob;
+      }
+      q.batch = i1 - i0;
+      if (i > 0) q.tail_counter = r.tail_counter ? tail_counter_slot() : nullptr;
+      e = b.launch(q, &used_tma);
+    }
+  } else {
+    const int rb = r.row_begin, re = r.row_end;
+    for (int64_t i = 0; i < parts && e == cudaSuccess; ++i) {
+      FusedLaunch q = r;
+      q.row_begin = rb + static_cast<int>((re - rb) * i / parts);
+      q.row_end = rb + static_cast<int>((re - rb) * (i + 1) / parts);
+      if (i > 0) q.tail_counter = r.tail_counter ? tail_counter_slot() : nullptr;
+      e = b.launch(q, &used_tma);
+    }
+  }
   if (e == cudaErrorNotSupported) return fail(B2DWT_EUNSUPPORTED, "no compiled fused variant for this request");
   if (e != cudaSuccess) return cuda_fail(e, "fused stream kernel");
   return B2DWT_OK;

@@ -287,3 +287,20 @@ def test_dwt_host_matches_golden_pyramids():
                 assert np.array_equal(band.numpy(), pyr[f"{base}/{lvl}/{name}"]), (base, lvl, name)
         checked += 1
     assert checked > 0
+
+
+def test_footprint_split_launches_bit_exact(monkeypatch):
+    """Requests above B2DWT_MAX_LAUNCH_BYTES run as row bands (one image) or
+    batch chunks; results must not change by a bit."""
+    tr = _golden_transform("cdf97", "non-separable-split", "single", tile=False)
+    x = torch.rand((2050, 3074), device="cuda")
+    xb = torch.rand((5, 130, 262), device="cuda")
+    whole = tr.forward(x)
+    whole_b = tr.forward(xb)
+    rec = tr.inverse(*whole)
+    monkeypatch.setenv("B2DWT_MAX_LAUNCH_BYTES", str(1 << 20))
+    for a, b in zip(tr.forward(x), whole):
+        assert torch.equal(a, b)
+    for a, b in zip(tr.forward(xb), whole_b):
+        assert torch.equal(a, b)
+    assert torch.equal(tr.inverse(*whole), rec)
