@@ -136,6 +136,17 @@ int b2dwt_forward_rows(b2dwt_plan plan, const void* image, int64_t image_ld, int
                        int64_t image_rows, int64_t global_height, int64_t width, int64_t out_row_begin,
                        int64_t out_row_end, const b2dwt_planes* out, void* stream);
 
+/* Row-band inverse (the mirror of b2dwt_forward_rows; `plan` holds the inverse
+ * program).  The four subband planes `in` hold quad rows [in_row0, in_row0 +
+ * in_rows) of a global_height x width image's subbands (row 0 of each plane is
+ * quad row in_row0); they must cover [out_row_begin - halo_up, out_row_end +
+ * halo_down) clipped to the image.  Writes pixel rows [2*out_row_begin,
+ * 2*out_row_end) to `image`, which points at pixel row 2*out_row_begin.
+ * Bit-identical to the same rows of b2dwt_inverse on the whole image. */
+int b2dwt_inverse_rows(b2dwt_plan plan, const b2dwt_planes* in, int64_t in_row0, int64_t in_rows, void* image,
+                       int64_t image_ld, int64_t global_height, int64_t width, int64_t out_row_begin,
+                       int64_t out_row_end, void* stream);
+
 /* Multi-level forward pyramid.  Level l (0-based) transforms the (H>>l) x (W>>l)
  * LL of level l-1 (level 0: `image`).  details[l] receives HL/LH/HH of level l
  * (ptr[0] ignored); `ll_out` (pitch ll_ld) receives the final LL, an
@@ -169,6 +180,16 @@ int64_t b2dwt_dwt_host_workspace(b2dwt_plan plan, int64_t height, int64_t width,
 int b2dwt_dwt_host(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t height, int64_t width,
                    int32_t levels, const b2dwt_planes* details, void* ll_out, int64_t ll_ld, void* workspace,
                    int64_t workspace_bytes, int32_t bands, void* stream);
+
+/* Multi-level inverse from HOST subbands into a HOST image (`plan` holds the
+ * inverse program): the coarse levels are uploaded and inverted whole, level 0
+ * runs in `bands` row bands with its upload, kernels and image download
+ * overlapped.  Host pointers as for b2dwt_dwt_host; `workspace` holds
+ * b2dwt_idwt_host_workspace() bytes.  Bit-identical to b2dwt_idwt. */
+int64_t b2dwt_idwt_host_workspace(b2dwt_plan plan, int64_t height, int64_t width, int32_t levels);
+int b2dwt_idwt_host(b2dwt_plan plan, const void* ll, int64_t ll_ld, const b2dwt_planes* details, int32_t levels,
+                    void* image, int64_t image_ld, int64_t height, int64_t width, void* workspace,
+                    int64_t workspace_bytes, int32_t bands, void* stream);
 
 #ifdef __cplusplus
 }

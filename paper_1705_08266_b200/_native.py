@@ -37,6 +37,9 @@ EXPORTS = (
     "b2dwt_idwt",
     "b2dwt_dwt_host_workspace",
     "b2dwt_dwt_host",
+    "b2dwt_inverse_rows",
+    "b2dwt_idwt_host_workspace",
+    "b2dwt_idwt_host",
 )
 
 
@@ -124,6 +127,9 @@ def load():
             "b2dwt_idwt": (ctypes.c_int, [vp, vp, i64, P(Planes), i32, vp, i64, i64, i64, vp, vp]),
             "b2dwt_dwt_host_workspace": (i64, [vp, i64, i64, i32]),
             "b2dwt_dwt_host": (ctypes.c_int, [vp, vp, i64, i64, i64, i32, P(Planes), vp, i64, vp, i64, i32, vp]),
+            "b2dwt_inverse_rows": (ctypes.c_int, [vp, P(Planes), i64, i64, vp, i64, i64, i64, i64, i64, vp]),
+            "b2dwt_idwt_host_workspace": (i64, [vp, i64, i64, i32]),
+            "b2dwt_idwt_host": (ctypes.c_int, [vp, vp, i64, P(Planes), i32, vp, i64, i64, i64, vp, i64, i32, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -716,6 +716,53 @@ int b2dwt_forward_rows(b2dwt_plan plan, const void* image, int64_t image_ld, int
   return run_fused(*plan, r);
 }
 
+int b2dwt_inverse_rows(b2dwt_plan plan, const b2dwt_planes* in, int64_t in_row0, int64_t in_rows, void* image,
+                       int64_t image_ld, int64_t global_height, int64_t width, int64_t out_row_begin,
+                       int64_t out_row_end, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (int rc = check_dims(global_height, width)) return rc;
+  if (!image) return fail(B2DWT_EINVAL, "null image");
+  if (int rc = check_planes(in, "input")) return rc;
+  const int64_t rows = global_height / 2, cols = width / 2;
+  if (in_row0 < 0 || in_rows < 1 || in_row0 + in_rows > rows)
+    return fail(B2DWT_EINVAL, "subband band must be a quad-row range inside the image");
+  if (out_row_begin < 0 || out_row_end > rows || out_row_begin >= out_row_end)
+    return fail(B2DWT_EINVAL, "bad output row range");
+  if (image_ld < width) return fail(B2DWT_EINVAL, "image_ld < width");
+  if (!fused_layout_ok(*plan, 1, 0))
+    return fail(B2DWT_EUNSUPPORTED, "row-band inverse needs a fused built-in inverse program");
+  const int64_t need0 = std::max<int64_t>(0, out_row_begin - plan->cone.up);
+  const int64_t need1 = std::min<int64_t>(rows, out_row_end + plan->cone.down);
+  if (need0 < in_row0 || need1 > in_row0 + in_rows) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "band holds quad rows [%lld,%lld) but rows [%lld,%lld) are needed",
+                  static_cast<long long>(in_row0), static_cast<long long>(in_row0 + in_rows),
+                  static_cast<long long>(need0), static_cast<long long>(need1));
+    return fail(B2DWT_EINVAL, buf);
+  }
+  FusedLaunch r{};
+  r.lin = 1;
+  r.lout = 0;
+  for (int c = 0; c < 4; ++c) {
+    r.in_pl[c] = in->ptr[c];
+    r.in_ld[c] = in->ld[c];
+  }
+  r.in_bstride = in->bstride;
+  r.in_row0 = static_cast<int>(in_row0);
+  r.in_rows = static_cast<int>(in_rows);
+  r.out_img = image;
+  r.out_ld[0] = image_ld;
+  r.out_bstride = image_ld * 2 * (out_row_end - out_row_begin);
+  r.out_row0 = static_cast<int>(out_row_begin);
+  r.rows = static_cast<int>(rows);
+  r.cols = static_cast<int>(cols);
+  r.row_begin = static_cast<int>(out_row_begin);
+  r.row_end = static_cast<int>(out_row_end);
+  r.batch = 1;
+  r.stream = static_cast<cudaStream_t>(stream);
+  return run_fused(*plan, r);
+}
+
 int b2dwt_dwt(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t height, int64_t width, int32_t levels,
               const b2dwt_planes* details, void* ll_out, int64_t ll_ld, void* scratch, void* stream) {
   if (int rc = check_plan(plan)) return rc;

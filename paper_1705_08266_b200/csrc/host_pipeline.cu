@@ -256,3 +256,172 @@ int b2dwt_dwt_host(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Inverse: host subbands -> host image.  The coarse levels (a quarter of the
+// data) are uploaded first and inverted whole; level 0 -- three quarters of the
+// input and all of the output -- runs in row bands: upload chunk k of its
+// HL/LH/HH (and LL when there is one level), invert rows as soon as the chunk
+// plus the cone is present, download the image rows while later chunks upload.
+
+namespace {
+
+struct InvLayout {
+  std::vector<size_t> det;  // HL/LH/HH of level l (three planes back to back)
+  std::vector<size_t> rec;  // image rebuilt by level l (l >= 1) = LL input of level l-1
+  size_t ll = 0;            // coarsest LL
+  size_t image = 0;
+  size_t total = 0;
+};
+
+InvLayout inv_layout_of(int64_t h, int64_t w, int levels, size_t es) {
+  InvLayout L;
+  size_t off = 0;
+  L.rec.assign(levels, 0);
+  for (int l = 0; l < levels; ++l) {
+    const size_t q = static_cast<size_t>((h >> (l + 1)) * (w >> (l + 1))) * es;
+    L.det.push_back(off);
+    off = align_up(off + 3 * align_up(q));
+    if (l >= 1) {
+      L.rec[l] = off;
+      off = align_up(off + static_cast<size_t>((h >> l) * (w >> l)) * es);
+    }
+  }
+  L.ll = off;
+  off = align_up(off + static_cast<size_t>((h >> levels) * (w >> levels)) * es);
+  L.image = off;
+  off = align_up(off + static_cast<size_t>(h * w) * es);
+  L.total = off;
+  return L;
+}
+
+cudaError_t h2d_rows(void* dst, int64_t dld, const void* src, int64_t sld, int64_t cols, int64_t r0, int64_t r1,
+                     size_t es, cudaStream_t s) {
+  if (r1 <= r0) return cudaSuccess;
+  return cudaMemcpy2DAsync(static_cast<char*>(dst) + static_cast<size_t>(r0 * dld) * es, dld * es,
+                           static_cast<const char*>(src) + static_cast<size_t>(r0 * sld) * es, sld * es, cols * es,
+                           r1 - r0, cudaMemcpyHostToDevice, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t b2dwt_idwt_host_workspace(b2dwt_plan plan, int64_t height, int64_t width, int32_t levels) {
+  b2dwt_plan_info info;
+  if (b2dwt_plan_get_info(plan, &info) != B2DWT_OK || levels < 1 || height < 2 || width < 2) return -1;
+  return static_cast<int64_t>(inv_layout_of(height, width, levels, info.dtype == B2DWT_F32 ? 4 : 8).total);
+}
+
+int b2dwt_idwt_host(b2dwt_plan plan, const void* ll, int64_t ll_ld, const b2dwt_planes* details, int32_t levels,
+                    void* image, int64_t image_ld, int64_t height, int64_t width, void* workspace,
+                    int64_t workspace_bytes, int32_t bands, void* stream) {
+  b2dwt_plan_info info;
+  if (int rc = b2dwt_plan_get_info(plan, &info)) return rc;
+  if (levels < 1) return pipe_fail(B2DWT_EINVAL, "levels must be >= 1");
+  if (!image || !details || !ll || !workspace) return pipe_fail(B2DWT_EINVAL, "null pointer");
+  if (height < 2 || width < 2 || (height % (2LL << (levels - 1))) || (width % (2LL << (levels - 1))))
+    return pipe_fail(B2DWT_EINVAL, "height and width must be divisible by 2^levels");
+  if (image_ld < width || ll_ld < (width >> levels)) return pipe_fail(B2DWT_EINVAL, "row pitch smaller than width");
+  if (info.kernel != 1 || std::strstr(info.key, "/inv") == nullptr)
+    return pipe_fail(B2DWT_EUNSUPPORTED, "host pipeline needs a fused built-in inverse program");
+  const size_t es = info.dtype == B2DWT_F32 ? 4 : 8;
+  const InvLayout L = inv_layout_of(height, width, levels, es);
+  if (workspace_bytes < static_cast<int64_t>(L.total)) return pipe_fail(B2DWT_EINVAL, "workspace too small");
+  if (reinterpret_cast<uintptr_t>(workspace) % kAlign) return pipe_fail(B2DWT_EINVAL, "workspace must be 256-B aligned");
+  char* ws = static_cast<char*>(workspace);
+  cudaStream_t s_comp = static_cast<cudaStream_t>(stream);
+  const int64_t R0 = height / 2, C0 = width / 2;
+  const int K = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(bands > 0 ? bands : 16, R0 / std::max<int64_t>(1, std::max(info.halo_up, info.halo_down)))));
+
+  Resources res;
+  res.timing = false;
+  cudaError_t e;
+  auto fail_e = [&](const char* what) { return pipe_fail(B2DWT_ECUDA, std::string(what) + cudaGetErrorString(e)); };
+  if ((e = cudaStreamCreateWithFlags(&res.s_in, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&res.s_out, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail_e("stream create: ");
+  cudaEvent_t ev_start, ev_coarse;
+  if ((e = res.event(&ev_start)) != cudaSuccess || (e = cudaEventRecord(ev_start, s_comp)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(res.s_in, ev_start, 0)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(res.s_out, ev_start, 0)) != cudaSuccess)
+    return fail_e("event: ");
+  auto det_plane = [&](int l, int c) {  // device plane c (1..3) of level l
+    const size_t q = static_cast<size_t>((height >> (l + 1)) * (width >> (l + 1))) * es;
+    return ws + L.det[l] + (c - 1) * align_up(q);
+  };
+  // 1. coarse levels: LL and details of levels >= 1, uploaded whole
+  const int64_t Rl = height >> levels, Cl = width >> levels;
+  if (levels > 1 && (e = h2d_rows(ws + L.ll, Cl, ll, ll_ld, Cl, 0, Rl, es, res.s_in)) != cudaSuccess)
+    return fail_e("H2D: ");
+  for (int l = levels - 1; l >= 1; --l) {
+    const int64_t R = height >> (l + 1), C = width >> (l + 1);
+    for (int c = 1; c < 4; ++c)
+      if ((e = h2d_rows(det_plane(l, c), C, details[l].ptr[c], details[l].ld[c], C, 0, R, es, res.s_in)) !=
+          cudaSuccess)
+        return fail_e("H2D: ");
+  }
+  if ((e = res.event(&ev_coarse)) != cudaSuccess || (e = cudaEventRecord(ev_coarse, res.s_in)) != cudaSuccess)
+    return fail_e("event: ");
+  // 2. level-0 inputs in K row chunks (LL too when there is a single level)
+  char* ll0 = levels > 1 ? ws + L.rec[1] : ws + L.ll;
+  std::vector<cudaEvent_t> ev_in(K);
+  std::vector<int64_t> chunk_end(K);
+  for (int k = 0; k < K; ++k) {
+    const int64_t r0 = R0 * k / K, r1 = R0 * (k + 1) / K;
+    chunk_end[k] = r1;
+    if (levels == 1 && (e = h2d_rows(ll0, C0, ll, ll_ld, C0, r0, r1, es, res.s_in)) != cudaSuccess)
+      return fail_e("H2D: ");
+    for (int c = 1; c < 4; ++c)
+      if ((e = h2d_rows(det_plane(0, c), C0, details[0].ptr[c], details[0].ld[c], C0, r0, r1, es, res.s_in)) !=
+          cudaSuccess)
+        return fail_e("H2D: ");
+    if ((e = res.event(&ev_in[k])) != cudaSuccess || (e = cudaEventRecord(ev_in[k], res.s_in)) != cudaSuccess)
+      return fail_e("event: ");
+  }
+  // 3. invert the coarse levels whole (LL of level l = image rebuilt by level l+1)
+  if ((e = cudaStreamWaitEvent(s_comp, ev_coarse, 0)) != cudaSuccess) return fail_e("wait: ");
+  for (int l = levels - 1; l >= 1; --l) {
+    const int64_t h = height >> l, w = width >> l, C = w / 2;
+    b2dwt_planes in;
+    in.ptr[0] = l == levels - 1 ? ws + L.ll : ws + L.rec[l + 1];
+    for (int c = 1; c < 4; ++c) in.ptr[c] = det_plane(l, c);
+    for (int c = 0; c < 4; ++c) in.ld[c] = C;
+    in.bstride = 0;
+    if (int rc = b2dwt_inverse(plan, &in, ws + L.rec[l], w, 0, h, w, 1, s_comp)) return rc;
+  }
+  // 4. level 0 in bands that end a cone short of their chunk; 5. downloads
+  char* dimg = ws + L.image;
+  b2dwt_planes in0;
+  in0.ptr[0] = ll0;
+  for (int c = 1; c < 4; ++c) in0.ptr[c] = det_plane(0, c);
+  for (int c = 0; c < 4; ++c) in0.ld[c] = C0;
+  in0.bstride = 0;
+  int64_t prev = 0;
+  for (int k = 0; k < K; ++k) {
+    const int64_t end = k == K - 1 ? R0 : std::max(prev, std::min<int64_t>(R0, chunk_end[k] - info.halo_down));
+    if ((e = cudaStreamWaitEvent(s_comp, ev_in[k], 0)) != cudaSuccess) return fail_e("wait: ");
+    if (end > prev) {
+      if (int rc = b2dwt_inverse_rows(plan, &in0, 0, R0, dimg + static_cast<size_t>(2 * prev * width) * es, width,
+                                      height, width, prev, end, s_comp))
+        return rc;
+      cudaEvent_t ev_b;
+      if ((e = res.event(&ev_b)) != cudaSuccess || (e = cudaEventRecord(ev_b, s_comp)) != cudaSuccess ||
+          (e = cudaStreamWaitEvent(res.s_out, ev_b, 0)) != cudaSuccess)
+        return fail_e("event: ");
+      e = cudaMemcpy2DAsync(static_cast<char*>(image) + static_cast<size_t>(2 * prev * image_ld) * es, image_ld * es,
+                            dimg + static_cast<size_t>(2 * prev * width) * es, width * es, width * es,
+                            2 * (end - prev), cudaMemcpyDeviceToHost, res.s_out);
+      if (e != cudaSuccess) return fail_e("D2H: ");
+    }
+    prev = end;
+  }
+  cudaEvent_t ev_done;
+  if ((e = res.event(&ev_done)) != cudaSuccess || (e = cudaEventRecord(ev_done, res.s_out)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(s_comp, ev_done, 0)) != cudaSuccess)
+    return fail_e("event: ");
+  return B2DWT_OK;
+}
+
+}  // extern "C"

@@ -501,6 +501,73 @@ class Transform:
         return out
 
 
+    def idwt_host(self, ll, details, out=None, bands: int = 16, stream=None, sync: bool = True):
+        """Host subbands -> host image (b2dwt_idwt_host): the inverse of
+        :meth:`dwt_host`, with level 0's upload, kernels and download
+        overlapped in row bands.  ``ll`` / ``details`` are CPU tensors or NumPy
+        arrays (pinned memory gives the overlap); returns a CPU tensor."""
+        torch = _require_cuda()
+
+        def host(a):
+            t = torch.from_numpy(np.ascontiguousarray(a)) if isinstance(a, np.ndarray) else a
+            if t.device.type != "cpu" or t.dim() != 2 or t.stride(1) != 1:
+                raise ValueError("idwt_host takes host (CPU) [H, W] planes with contiguous rows")
+            if t.dtype != self.torch_dtype:
+                raise TypeError(f"expected {self.torch_dtype}, got {t.dtype}")
+            return t
+
+        ll = host(ll)
+        details = [tuple(host(b) for b in d) for d in details]
+        levels = len(details)
+        if levels < 1:
+            raise ValueError("levels must be >= 1")
+        h, w = ll.shape[0] << levels, ll.shape[1] << levels
+        for lvl, d in enumerate(details):
+            for b in d:
+                if tuple(b.shape) != (h >> (lvl + 1), w >> (lvl + 1)):
+                    raise ValueError("all four subbands must share dimensions")
+        if out is None:
+            out = torch.empty((h, w), dtype=ll.dtype, pin_memory=ll.is_pinned())
+        lib = _native.load()
+        need = int(lib.b2dwt_idwt_host_workspace(self.inv_plan.handle, h, w, levels))
+        if need < 0:
+            raise ValueError("bad idwt_host geometry")
+        ws = getattr(self, "_host_iws", None)
+        if ws is None or ws.numel() < need:
+            ws = torch.empty((need,), dtype=torch.uint8, device="cuda")
+            self._host_iws = ws
+        arr = (_native.Planes * levels)()
+        for lvl, (hl, lh, hh) in enumerate(details):
+            arr[lvl] = _native.planes([0, _ptr(hl), _ptr(lh), _ptr(hh)],
+                                      [0, hl.stride(0), lh.stride(0), hh.stride(0)], 0)
+        _native.check(
+            lib.b2dwt_idwt_host(self.inv_plan.handle, _ptr(ll), ll.stride(0), arr, levels, _ptr(out), out.stride(0),
+                                h, w, _ptr(ws), ws.numel(), bands, _stream_handle(torch, stream)),
+            "idwt_host",
+        )
+        if sync:
+            (stream if stream is not None else torch.cuda.current_stream()).synchronize()
+        return out
+
+    def inverse_rows(self, band, band_row0, global_height, out_row_begin, out_row_end, out=None, stream=None):
+        """Image rows [2*out_row_begin, 2*out_row_end) of the inverse from a row
+        band of the four subband planes (quad rows [band_row0, band_row0 +
+        rows)); mirror of :meth:`forward_rows` (b2dwt_inverse_rows)."""
+        torch = _torch()
+        ll = band[0]
+        w = 2 * ll.shape[1]
+        if out is None:
+            out = torch.empty((2 * (out_row_end - out_row_begin), w), dtype=ll.dtype, device=ll.device)
+        pin = _native.planes([_ptr(b) for b in band], [b.stride(0) for b in band], 0)
+        _native.check(
+            _native.load().b2dwt_inverse_rows(self.inv_plan.handle, pin, band_row0, ll.shape[0], _ptr(out),
+                                              out.stride(0), global_height, w, out_row_begin, out_row_end,
+                                              _stream_handle(torch, stream)),
+            "inverse_rows",
+        )
+        return out
+
+
 class PyramidGraph:
     """A multi-level forward transform captured as one CUDA graph.
 
@@ -654,5 +721,10 @@ def idwt(pyramid: Pyramid, scheme, cfg: TileConfig | None = None) -> Image2D:
     """Invert :func:`dwt` level by level, coarsest first."""
     torch = _require_cuda()
     tr = _transform(scheme, pyramid.ll.precision)
+    levels = len(pyramid.details)
+    if tr.inv_plan.fused and pyramid.ll.data.size << (2 * levels) >= _HOST_PIPELINE_MIN_PX:
+        # large host pyramid: level 0's upload, kernels and download overlapped
+        out = tr.idwt_host(pyramid.ll.data, [tuple(b.data for b in d) for d in pyramid.details])
+        return Image2D(out.numpy())
     details = [tuple(_to_device(torch, b.data) for b in d) for d in pyramid.details]
     return Image2D(_to_host(tr.idwt(_to_device(torch, pyramid.ll.data), details)))

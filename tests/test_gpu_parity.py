@@ -304,3 +304,38 @@ def test_footprint_split_launches_bit_exact(monkeypatch):
     for a, b in zip(tr.forward(xb), whole_b):
         assert torch.equal(a, b)
     assert torch.equal(tr.inverse(*whole), rec)
+
+
+@pytest.mark.parametrize("shape,levels,bands,pinned", [
+    ((1024, 768), 3, 16, True),
+    ((512, 1024), 1, 7, False),
+    ((2048, 2048), 5, 32, True),
+])
+def test_idwt_host_pipeline_equals_device(shape, levels, bands, pinned):
+    for wavelet in ("cdf53", "cdf97"):
+        tr = _golden_transform(wavelet, "non-separable-split", "single")
+        h, w = shape
+        x = torch.rand((h, w), device="cuda")
+        ll, det = tr.dwt(x, levels)
+        want = tr.idwt(ll, det).cpu()
+        hl = ll.cpu()
+        hd = [tuple(b.cpu() for b in d) for d in det]
+        if pinned:
+            hl = hl.pin_memory()
+            hd = [tuple(b.pin_memory() for b in d) for d in hd]
+        got = tr.idwt_host(hl, hd, bands=bands)
+        assert got.device.type == "cpu" and torch.equal(got, want), (wavelet, shape, levels)
+
+
+def test_inverse_rows_band_equals_full():
+    tr = _golden_transform("cdf97", "non-separable-split", "single")
+    x = torch.rand((512, 300), device="cuda")
+    q = tr.forward(x)
+    full = tr.inverse(*q)
+    up, down = tr.inv_plan.cone[0], tr.inv_plan.cone[1]
+    rows = 256
+    for (r0, r1) in [(0, 64), (64, 128), (200, 256), (17, 93)]:
+        b0, b1 = max(0, r0 - up), min(rows, r1 + down)
+        band = tuple(c[b0:b1].contiguous() for c in q)
+        got = tr.inverse_rows(band, b0, 512, r0, r1)
+        assert torch.equal(got, full[2 * r0:2 * r1]), (r0, r1)

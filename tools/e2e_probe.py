@@ -40,3 +40,10 @@ print(f"PCIe floor (1 GiB each way, concurrent): {timed(floor):.2f} ms", flush=T
 for b in [int(x) for x in os.environ.get("BANDS", "4 8 16 32 64").split()]:
     ms = timed(lambda: tr.dwt_host(host, levels, details=det, ll=ll, bands=b, sync=False))
     print(f"bands={b}: {ms:.2f} ms = {n * n / ms / 1e6:.2f} Gpx/s", flush=True)
+
+# inverse: host pyramid -> host image
+rec = torch.empty((n, n)).pin_memory()
+tr.dwt_host(host, levels, details=det, ll=ll, bands=16)
+for b in (8, 16, 32):
+    ms = timed(lambda: tr.idwt_host(ll, det, out=rec, bands=b, sync=False))
+    print(f"idwt_host bands={b}: {ms:.2f} ms = {n * n / ms / 1e6:.2f} Gpx/s", flush=True)
