@@ -191,6 +191,24 @@ int b2dwt_idwt_host(b2dwt_plan plan, const void* ll, int64_t ll_ld, const b2dwt_
                     void* image, int64_t image_ld, int64_t height, int64_t width, void* workspace,
                     int64_t workspace_bytes, int32_t bands, void* stream);
 
+/* Batched 1-D lifting (schemes.py:806-856 apply_plan_1d / invert_plan_1d) on
+ * `batch` signals of `length` (even) samples, row pitch *_ld in elements.
+ * Steps are applied in order; step s updates the odd/high plane (target 1,
+ * reading the even samples) or the even/low plane (target 0, reading the odd
+ * samples) with step_count[s] terms (shift k, coefficient c) in ascending k:
+ * x[i] += c * other[ext(i - k)], whole-sample symmetric extension.  Forward:
+ * split, steps, then multiply by scale = {lo, hi} (NULL: none).  Inverse
+ * (b2dwt_unlift1d, in place in low/high): divide by scale, the steps as given
+ * (the caller passes them reversed and negated), then merge.  f64 is
+ * bit-identical to the reference's Python floats. */
+int b2dwt_lift1d(int32_t dtype, int32_t n_steps, const int32_t* step_target, const int32_t* step_count,
+                 const int32_t* shifts, const double* coefs, const double* scale, const void* signal,
+                 int64_t signal_ld, void* low, void* high, int64_t out_ld, int64_t length, int32_t batch,
+                 void* stream);
+int b2dwt_unlift1d(int32_t dtype, int32_t n_steps, const int32_t* step_target, const int32_t* step_count,
+                   const int32_t* shifts, const double* coefs, const double* scale, void* low, void* high,
+                   int64_t band_ld, void* signal, int64_t signal_ld, int64_t length, int32_t batch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

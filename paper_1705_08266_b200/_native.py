@@ -40,6 +40,8 @@ EXPORTS = (
     "b2dwt_inverse_rows",
     "b2dwt_idwt_host_workspace",
     "b2dwt_idwt_host",
+    "b2dwt_lift1d",
+    "b2dwt_unlift1d",
 )
 
 
@@ -129,6 +131,8 @@ def load():
             "b2dwt_dwt_host": (ctypes.c_int, [vp, vp, i64, i64, i64, i32, P(Planes), vp, i64, vp, i64, i32, vp]),
             "b2dwt_inverse_rows": (ctypes.c_int, [vp, P(Planes), i64, i64, vp, i64, i64, i64, i64, i64, vp]),
             "b2dwt_idwt_host_workspace": (i64, [vp, i64, i64, i32]),
+            "b2dwt_lift1d": (ctypes.c_int, [i32, i32, vp, vp, vp, vp, vp, vp, i64, vp, vp, i64, i64, i32, vp]),
+            "b2dwt_unlift1d": (ctypes.c_int, [i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, vp, i64, i64, i32, vp]),
             "b2dwt_idwt_host": (ctypes.c_int, [vp, vp, i64, P(Planes), i32, vp, i64, i64, i64, vp, i64, i32, vp]),
         }
         for name, (res, args) in sig.items():

@@ -3,6 +3,7 @@
 Translation units:
   csrc/b2dwt_host.cu        C ABI, plan matching, generic interpreter kernel
   csrc/host_pipeline.cu     b2dwt_dwt_host: host-buffer pyramid, copies overlapped in row bands
+  csrc/lift1d.cu            batched 1-D lifting (b2dwt_lift1d / b2dwt_unlift1d)
   csrc/prog_dispatch.cu     per built-in program: variant selection, cone
   csrc/prog_variant.cu      ONE fused kernel per unit (program x element type x
                             layout x arithmetic x fill), compiled in parallel
@@ -99,7 +100,7 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
     # host TU in C++17 (nvcc 12.9's C++20 front end trips over libstdc++ 13
     # containers); kernel TUs need C++20 for the phase-unrolled tick loop
     tasks = [(os.path.join(CSRC, f"{u}.cu"), os.path.join(BUILD, f"{u}.o"), ["-std=c++17"],
-              os.path.join(BUILD, f"ptxas_{u}.log")) for u in ("b2dwt_host", "host_pipeline")]
+              os.path.join(BUILD, f"ptxas_{u}.log")) for u in ("b2dwt_host", "host_pipeline", "lift1d")]
     # dev builds: B2DWT_PROGRAMS=ident,... and/or B2DWT_VARIANTS=0,1 compile
     # only that subset; the rest are stubs (the host falls back to the generic
     # interpreter for them).  Release builds compile everything.

@@ -27,7 +27,7 @@ def lib():
 def test_exports_every_declared_symbol(lib):
     with open(os.path.join(ROOT, "include", "b2dwt.h")) as fh:
         header = fh.read()
-    declared = set(re.findall(r"\b(b2dwt_[a-z_]+)\s*\(", header))
+    declared = set(re.findall(r"\b(b2dwt_[a-z0-9_]+)\s*\(", header))
     assert declared == set(_native.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
