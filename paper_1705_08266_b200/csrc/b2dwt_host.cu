@@ -227,6 +227,26 @@ size_t esize(int dtype) { return dtype == B2DWT_F32 ? 4 : 8; }
 
 // ---------------------------------------------------------------------------
 // Generic path: one interpreter launch per sub-step, ping-pong scratch.
+
+// Stream-ordered scratch comes from the device's default memory pool; by
+// default the pool returns freed memory to the OS at every synchronisation, so
+// each call would map its scratch afresh (milliseconds for a 4096^2 image).
+// Keep it cached instead (once per device).
+void keep_pool_memory() {
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~uint64_t{0};
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  (void)cudaGetLastError();
+  done[dev] = true;
+}
 struct ViewSet {
   const void* p[4];
   int64_t rs[4], cs[4];
@@ -296,6 +316,7 @@ int run_generic(const b2dwt_plan_s& p, const ViewSet& in, int64_t in_b, const Vi
   const int64_t plane = rows * cols;
   void* scratch = nullptr;
   if (p.nsub > 1) {
+    keep_pool_memory();
     const size_t bytes = static_cast<size_t>(2 * 4 * plane * batch) * es;
     cudaError_t e = cudaMallocAsync(&scratch, bytes, stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(generic scratch)");

@@ -52,8 +52,10 @@ __global__ void __launch_bounds__(256)
       for (int j = 0; j < sub.count[t]; ++j, ++k) {
         const GenericTerm& g = sub.terms[k];
         const int s = g.src;
-        const int rr = reflect(n + g.dn, row_parity(s), rows);
-        const int cc = reflect(m + g.dm, col_parity(s), cols);
+        // reflection (a periodic map with divisions) only for reads outside the image
+        const int rn = n + g.dn, cm = m + g.dm;
+        const int rr = static_cast<unsigned>(rn) < static_cast<unsigned>(rows) ? rn : reflect(rn, row_parity(s), rows);
+        const int cc = static_cast<unsigned>(cm) < static_cast<unsigned>(cols) ? cm : reflect(cm, col_parity(s), cols);
         const T x = in[s].p[b * in_bstride + rr * in[s].rs + cc * in[s].cs];
         const T c = static_cast<T>(g.coeff);
         acc = (j == 0) ? Ar::mul(x, c) : Ar::mac(acc, x, c);
