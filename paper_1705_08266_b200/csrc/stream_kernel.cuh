@@ -930,8 +930,15 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
     const int64_t e = (s < s0 ? s : s0) + (s > s1 ? s - s1 : 0);
     return e * we + (s - e) * wi;
   };
-  const int64_t item_cost = super_cost0(n_super) * rows_out;
-  const int64_t total = item_cost * a.batch;
+  // Batches with uniform strip cost: super-strips run over the flattened
+  // (item, strip) sequence, so an image's last, partial super-strip is topped
+  // up with the next image's first strips instead of idling warps (2048^2
+  // images: 19 strips per item = 4 full super-strips + 3 strips).
+  const bool span = a.batch > 1 && we == wi;
+  const int64_t n_gstrips = static_cast<int64_t>(a.batch) * a.n_strips;
+  const int64_t item_cost = span ? wi * rows_out * ((n_gstrips + WARPS - 1) / WARPS)
+                                 : super_cost0(n_super) * rows_out;
+  const int64_t total = span ? item_cost : item_cost * a.batch;
   // Two tiers: [0, static_end) is split evenly over the resident CTAs (long
   // pipelines, no atomics); the tail is claimed in small chunks per CTA through
   // an atomic counter, so SMs that run faster absorb more of it.
@@ -955,11 +962,13 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
   for (;;) {
 #pragma unroll 1
   while (f < f_end) {
-    const int b = static_cast<int>(f / item_cost);
+    int b = span ? 0 : static_cast<int>(f / item_cost);
     const int64_t fi = f - b * item_cost;
     // super-strip containing cost offset fi (piecewise-linear inverse of super_cost0)
     int sup;
-    {
+    if (span) {
+      sup = static_cast<int>(fi / (wi * rows_out));
+    } else {
       const int64_t c_s0 = static_cast<int64_t>(s0) * we * rows_out;
       const int64_t c_s1 = super_cost0(s1) * rows_out;
       if (fi < c_s0)
@@ -970,14 +979,20 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
         sup = s1 + static_cast<int>((fi - c_s1) / (we * rows_out));
       if (sup >= n_super) sup = n_super - 1;
     }
-    const bool edge_super = sup < s0 || sup >= s1;
+    const bool edge_super = !span && (sup < s0 || sup >= s1);
     const int64_t wr = edge_super ? we : wi;
-    const int64_t c0 = b * item_cost + super_cost0(sup) * rows_out;  // cost of row 0 of this super-strip
+    const int64_t c0 = span ? wi * rows_out * sup : b * item_cost + super_cost0(sup) * rows_out;  // cost of row 0
     // rows whose start cost lies in [f, f_end)
     const int r0 = static_cast<int>((f - c0 + wr - 1) / wr);
     const int r1 = static_cast<int>(min(static_cast<int64_t>(rows_out), (f_end - c0 + wr - 1) / wr));
     f = c0 + wr * rows_out;  // next super-strip
-    const int strip = sup * WARPS + warp;
+    int strip = sup * WARPS + warp;
+    if (span) {  // global strip -> (item, strip)
+      const int64_t g = static_cast<int64_t>(sup) * WARPS + warp;
+      if (g >= n_gstrips) continue;
+      b = static_cast<int>(g / a.n_strips);
+      strip = static_cast<int>(g - static_cast<int64_t>(b) * a.n_strips);
+    }
     if (r0 >= r1 || strip >= a.n_strips) continue;
     const int r = r0;
     const int seg_len = r1 - r0;
