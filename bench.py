@@ -349,7 +349,8 @@ def run_c3(args):
             },
             "roofline": {
                 "bound": "hbm",
-                "kernel": "stream_kernel<cdf97_nssplit_fwd, f32> level 0 (16384^2 -> 4 x 8192^2)",
+                "kernel": "stream_kernel<cdf97_nssplit_fwd, f32> level 0 (16384^2 -> 4 x 8192^2; two "
+                          "footprint-bounded launches of 4096 quad rows, achieved/traffic per level)",
                 "achieved": achieved,
                 "peak": peak,
                 "peak_source": peak_src,
