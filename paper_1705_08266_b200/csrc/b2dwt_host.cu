@@ -20,6 +20,7 @@
 
 #include "../../include/b2dwt.h"
 #include "generic_kernel.cuh"
+#include "generic_tile.cuh"
 #include "launch.h"
 
 namespace b2dwt {
@@ -347,7 +348,108 @@ int run_generic(const b2dwt_plan_s& p, const ViewSet& in, int64_t in_b, const Vi
   return B2DWT_OK;
 }
 
+void keep_pool_memory();
+
 // ---------------------------------------------------------------------------
+// Fused generic interpreter (generic_tile.cuh) for plans without a built-in
+// kernel: B2DWT_EUNSUPPORTED when the program does not fit it (the caller
+// then runs the per-sub-step interpreter).
+template <class T>
+cudaError_t launch_gtile(const b2dwt_plan_s& p, const GTileProgram& g, const FusedLaunch& r) {
+  GTileArgs<T> a{};
+  a.in_img = static_cast<const T*>(r.in_img);
+  for (int c = 0; c < 4; ++c) {
+    a.in_pl[c] = static_cast<const T*>(r.in_pl[c]);
+    a.out_pl[c] = static_cast<T*>(r.out_pl[c]);
+    a.in_ld[c] = r.in_ld[c];
+    a.out_ld[c] = r.out_ld[c];
+  }
+  a.in_bstride = r.in_bstride;
+  a.out_img = static_cast<T*>(r.out_img);
+  a.out_bstride = r.out_bstride;
+  a.lin = r.lin;
+  a.lout = r.lout;
+  a.rows = r.rows;
+  a.cols = r.cols;
+  a.batch = r.batch;
+  a.tr = kGTileWR - g.up - g.down;
+  a.tc = kGTileWC - g.left - g.right;
+  a.tiles_r = (r.rows + a.tr - 1) / a.tr;
+  a.tiles_c = (r.cols + a.tc - 1) / a.tc;
+  const int64_t n = static_cast<int64_t>(a.tiles_r) * a.tiles_c * r.batch;
+  if (n > 0x7fffffff) return cudaErrorNotSupported;
+  const size_t smem = gtile_smem_bytes(sizeof(T));
+  // the term table travels in stream-ordered device memory (too large for the
+  // parameter block); the pool keeps it cached between calls
+  keep_pool_memory();
+  void* dg = nullptr;
+  cudaError_t e = cudaMallocAsync(&dg, sizeof(GTileProgram), r.stream);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(dg, &g, sizeof(GTileProgram), cudaMemcpyHostToDevice, r.stream);
+  if (e == cudaSuccess) {
+    if (strict_of(&p)) {
+      e = cudaFuncSetAttribute(generic_tile_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem));
+      if (e == cudaSuccess)
+        generic_tile_kernel<T, true><<<static_cast<unsigned>(n), kGTileThreads, smem, r.stream>>>(
+            a, static_cast<const GTileProgram*>(dg));
+    } else {
+      e = cudaFuncSetAttribute(generic_tile_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem));
+      if (e == cudaSuccess)
+        generic_tile_kernel<T, false><<<static_cast<unsigned>(n), kGTileThreads, smem, r.stream>>>(
+            a, static_cast<const GTileProgram*>(dg));
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+  }
+  cudaFreeAsync(dg, r.stream);
+  return e;
+}
+
+int try_gtile(const b2dwt_plan_s& p, const FusedLaunch& r) {
+  if ((p.flags & B2DWT_NO_TILE) || p.builtin >= 0 && !(p.flags & B2DWT_FORCE_GENERIC)) return B2DWT_EUNSUPPORTED;
+  if (p.nsub > kGTileMaxSub || static_cast<int>(p.terms.size()) > kGTileMaxTerms) return B2DWT_EUNSUPPORTED;
+  GTileProgram g{};
+  g.n_sub = p.nsub;
+  int k = 0;
+  for (int s = 0; s < p.nsub; ++s) {
+    int ru = 0, rd = 0, rl = 0, rr = 0;
+    for (int t = 0; t < 4; ++t) {
+      const int n = p.counts[s * 4 + t];
+      g.count[s][t] = static_cast<int16_t>(n);
+      g.first[s][t] = static_cast<int16_t>(k);
+      for (int j = 0; j < n; ++j, ++k) {
+        const b2dwt_term& tm = p.terms[k];
+        if (tm.dn < -kGTileMaxReach || tm.dn > kGTileMaxReach || tm.dm < -kGTileMaxReach ||
+            tm.dm > kGTileMaxReach)
+          return B2DWT_EUNSUPPORTED;
+        g.src[k] = static_cast<int16_t>(tm.src);
+        g.off[k] = static_cast<int16_t>(tm.dn * kGTileWC + tm.dm);
+        g.unit[k] = tm.coeff == 1.0;  // x * 1.0 == x: skipping it is exact
+        g.coef[k] = tm.coeff;
+        ru = std::max(ru, -tm.dn);
+        rd = std::max(rd, tm.dn);
+        rl = std::max(rl, -tm.dm);
+        rr = std::max(rr, tm.dm);
+      }
+      const b2dwt_term* t0 = n == 1 ? &p.terms[k - 1] : nullptr;
+      g.identity[s][t] = t0 && t0->src == t && t0->dm == 0 && t0->dn == 0 && t0->coeff == 1.0;
+    }
+    g.up += ru;
+    g.down += rd;
+    g.left += rl;
+    g.right += rr;
+  }
+  // the window must leave an output tile, and every ghost cell inside the
+  // output's cone must mirror a cell inside the window (near-symmetric cone)
+  if (kGTileWR - g.up - g.down < 2 || kGTileWC - g.left - g.right < 2) return B2DWT_EUNSUPPORTED;
+  if (std::abs(g.up - g.down) > 1 || std::abs(g.left - g.right) > 1) return B2DWT_EUNSUPPORTED;
+  const cudaError_t e = p.dtype == B2DWT_F32 ? launch_gtile<float>(p, g, r) : launch_gtile<double>(p, g, r);
+  if (e == cudaErrorNotSupported) return B2DWT_EUNSUPPORTED;
+  if (e != cudaSuccess) return cuda_fail(e, "generic tile kernel");
+  return B2DWT_OK;
+}
+
 int run_fused(const b2dwt_plan_s& p, FusedLaunch& r) {
   const Builtin& b = builtins()[p.builtin];
   r.dtype = p.dtype;
@@ -586,30 +688,31 @@ int b2dwt_run_components(b2dwt_plan plan, const b2dwt_planes* in, const b2dwt_pl
   if (rows < 1 || cols < 1 || batch < 1) return fail(B2DWT_EINVAL, "empty component grid");
   if (int rc = check_dims(2 * rows, 2 * cols)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  FusedLaunch r{};
+  r.lin = 1;
+  r.lout = 1;
+  for (int c = 0; c < 4; ++c) {
+    r.in_pl[c] = in->ptr[c];
+    r.out_pl[c] = out->ptr[c];
+  }
+  for (int c = 0; c < 4; ++c) {
+    r.in_ld[c] = in->ld[c];
+    r.out_ld[c] = out->ld[c];
+  }
+  r.in_bstride = in->bstride;
+  r.in_rows = static_cast<int>(rows);
+  r.out_bstride = out->bstride;
+  r.rows = static_cast<int>(rows);
+  r.cols = static_cast<int>(cols);
+  r.row_begin = 0;
+  r.row_end = static_cast<int>(rows);
+  r.batch = batch;
+  r.stream = s;
   if (fused_layout_ok(*plan, 1, 1)) {
-    FusedLaunch r{};
-    r.lin = 1;
-    r.lout = 1;
-    for (int c = 0; c < 4; ++c) {
-      r.in_pl[c] = in->ptr[c];
-      r.out_pl[c] = out->ptr[c];
-    }
-    for (int c = 0; c < 4; ++c) {
-      r.in_ld[c] = in->ld[c];
-      r.out_ld[c] = out->ld[c];
-    }
-    r.in_bstride = in->bstride;
-    r.in_rows = static_cast<int>(rows);
-    r.out_bstride = out->bstride;
-    r.rows = static_cast<int>(rows);
-    r.cols = static_cast<int>(cols);
-    r.row_begin = 0;
-    r.row_end = static_cast<int>(rows);
-    r.batch = batch;
-    r.stream = s;
     const int rc = run_fused(*plan, r);
     if (rc != B2DWT_EUNSUPPORTED) return rc;
   }
+  if (int rc = try_gtile(*plan, r); rc != B2DWT_EUNSUPPORTED) return rc;
   const size_t es = esize(plan->dtype);
   return run_generic(*plan, planar_views(in, es), in->bstride, planar_views(out, es), out->bstride, rows, cols,
                      batch, s);
@@ -625,28 +728,29 @@ int b2dwt_forward(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t 
   if (image_ld < width) return fail(B2DWT_EINVAL, "image_ld < width");
   const int64_t rows = height / 2, cols = width / 2;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  FusedLaunch r{};
+  r.lin = 0;
+  r.lout = 1;
+  r.in_img = image;
+  r.in_ld[0] = image_ld;
+  r.in_bstride = image_bstride;
+  r.in_rows = static_cast<int>(rows);
+  for (int c = 0; c < 4; ++c) {
+    r.out_pl[c] = out->ptr[c];
+    r.out_ld[c] = out->ld[c];
+  }
+  r.out_bstride = out->bstride;
+  r.rows = static_cast<int>(rows);
+  r.cols = static_cast<int>(cols);
+  r.row_begin = 0;
+  r.row_end = static_cast<int>(rows);
+  r.batch = batch;
+  r.stream = s;
   if (fused_layout_ok(*plan, 0, 1)) {
-    FusedLaunch r{};
-    r.lin = 0;
-    r.lout = 1;
-    r.in_img = image;
-    r.in_ld[0] = image_ld;
-    r.in_bstride = image_bstride;
-    r.in_rows = static_cast<int>(rows);
-    for (int c = 0; c < 4; ++c) {
-      r.out_pl[c] = out->ptr[c];
-      r.out_ld[c] = out->ld[c];
-    }
-    r.out_bstride = out->bstride;
-    r.rows = static_cast<int>(rows);
-    r.cols = static_cast<int>(cols);
-    r.row_begin = 0;
-    r.row_end = static_cast<int>(rows);
-    r.batch = batch;
-    r.stream = s;
     const int rc = run_fused(*plan, r);
     if (rc != B2DWT_EUNSUPPORTED) return rc;
   }
+  if (int rc = try_gtile(*plan, r); rc != B2DWT_EUNSUPPORTED) return rc;
   const size_t es = esize(plan->dtype);
   return run_generic(*plan, image_views(image, image_ld, es), image_bstride, planar_views(out, es), out->bstride,
                      rows, cols, batch, s);
@@ -662,28 +766,29 @@ int b2dwt_inverse(b2dwt_plan plan, const b2dwt_planes* in, void* image, int64_t 
   if (image_ld < width) return fail(B2DWT_EINVAL, "image_ld < width");
   const int64_t rows = height / 2, cols = width / 2;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  FusedLaunch r{};
+  r.lin = 1;
+  r.lout = 0;
+  for (int c = 0; c < 4; ++c) {
+    r.in_pl[c] = in->ptr[c];
+    r.in_ld[c] = in->ld[c];
+  }
+  r.in_bstride = in->bstride;
+  r.in_rows = static_cast<int>(rows);
+  r.out_img = image;
+  r.out_ld[0] = image_ld;
+  r.out_bstride = image_bstride;
+  r.rows = static_cast<int>(rows);
+  r.cols = static_cast<int>(cols);
+  r.row_begin = 0;
+  r.row_end = static_cast<int>(rows);
+  r.batch = batch;
+  r.stream = s;
   if (fused_layout_ok(*plan, 1, 0)) {
-    FusedLaunch r{};
-    r.lin = 1;
-    r.lout = 0;
-    for (int c = 0; c < 4; ++c) {
-      r.in_pl[c] = in->ptr[c];
-      r.in_ld[c] = in->ld[c];
-    }
-    r.in_bstride = in->bstride;
-    r.in_rows = static_cast<int>(rows);
-    r.out_img = image;
-    r.out_ld[0] = image_ld;
-    r.out_bstride = image_bstride;
-    r.rows = static_cast<int>(rows);
-    r.cols = static_cast<int>(cols);
-    r.row_begin = 0;
-    r.row_end = static_cast<int>(rows);
-    r.batch = batch;
-    r.stream = s;
     const int rc = run_fused(*plan, r);
     if (rc != B2DWT_EUNSUPPORTED) return rc;
   }
+  if (int rc = try_gtile(*plan, r); rc != B2DWT_EUNSUPPORTED) return rc;
   const size_t es = esize(plan->dtype);
   return run_generic(*plan, planar_views(in, es), in->bstride, image_views(image, image_ld, es), image_bstride,
                      rows, cols, batch, s);

@@ -63,10 +63,15 @@ def _host(t):
     return t.cpu().numpy()
 
 
-VARIANTS = [dict(tile=False), dict(tile=False, tma=False), dict(tile=True), dict(force_generic=True)]
+# stream / tile: the built-in kernels (custom plans: tile=False -> per-sub-step
+# interpreter, otherwise the fused generic tile kernel); generic-*: built-ins
+# forced through the runtime-programmed kernels
+VARIANTS = [dict(tile=False), dict(tile=False, tma=False), dict(tile=True), dict(force_generic=True),
+            dict(force_generic=True, tile=False)]
 
 
-@pytest.mark.parametrize("variant", VARIANTS, ids=["stream-tma", "stream-cpasync", "tile", "generic"])
+@pytest.mark.parametrize("variant", VARIANTS,
+                         ids=["stream-tma", "stream-cpasync", "tile", "generic-tile", "generic-substep"])
 def test_vectors_bit_exact(variant):
     vec = G.vectors()
     checked = 0
