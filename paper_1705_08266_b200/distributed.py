@@ -150,6 +150,71 @@ class RowStrips:
         for e in edges:
             self._run_band(band_forward, buf, level, e, out)
 
+    # -- inverse -----------------------------------------------------------------
+    # The inverse strips the four subband planes instead: rank r owns quad rows
+    # [row0/2, (row0+rows)/2) of every plane plus `up` / `down` halo quad rows of
+    # the INVERSE program's cone (construct the RowStrips with
+    # Transform.inv_plan.cone[:2]), exchanged per plane; bands go through
+    # ``band_inverse`` = Transform.inverse_rows, which reflects only at global
+    # edges, so the image rows are bit-identical to the single-GPU inverse.
+
+    def _sub_halos(self):
+        return (self.up if self.rank > 0 else 0), (self.down if self.rank < self.world - 1 else 0)
+
+    def allocate_subbands(self, new_empty, level: int = 0):
+        """[4, halo_top + owned + halo_bot quad rows, W/2] buffer of the planes."""
+        L = self.layout(level)
+        ht, hb = self._sub_halos()
+        return new_empty((4, ht + L.rows // 2 + hb, L.width // 2))
+
+    def owned_subbands(self, sb, level: int = 0):
+        ht, _ = self._sub_halos()
+        return sb[:, ht:ht + self.layout(level).rows // 2]
+
+    def exchange_subbands(self, sb, level: int = 0, group=None):
+        """Post the per-plane halo send/recv of a subband buffer; returns the requests."""
+        import torch.distributed as dist
+
+        q = self.layout(level).rows // 2
+        ht, hb = self._sub_halos()
+        ops = []
+        for c in range(4):
+            own = sb[c, ht:ht + q]
+            if self.rank > 0:
+                ops.append(dist.P2POp(dist.irecv, sb[c, :ht], self.rank - 1, group))
+                ops.append(dist.P2POp(dist.isend, own[:self.down].contiguous(), self.rank - 1, group))
+            if self.rank < self.world - 1:
+                ops.append(dist.P2POp(dist.isend, own[q - self.up:].contiguous(), self.rank + 1, group))
+                ops.append(dist.P2POp(dist.irecv, sb[c, ht + q:], self.rank + 1, group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def _run_inverse_band(self, band_inverse, sb, level, out_rows, out):
+        L = self.layout(level)
+        r0, r1 = out_rows
+        if r1 <= r0:
+            return
+        q0 = L.quad_rows[0]
+        buf_q0 = q0 - self._sub_halos()[0]  # global quad row of buffer row 0
+        b0 = max(0, r0 - self.up)
+        b1 = min(L.height // 2, r1 + self.down)
+        band = tuple(sb[c, b0 - buf_q0:b1 - buf_q0] for c in range(4))
+        band_inverse(band, b0, L.height, r0, r1, out[2 * (r0 - q0):2 * (r1 - q0)])
+
+    def inverse(self, band_inverse, sb, out, level: int = 0, group=None, overlap: bool = True):
+        """One level of the inverse: exchange the planes' halos and rebuild the
+        owned image rows into ``out`` ([rows, W])."""
+        interior, edges = self._bands(level)
+        reqs = self.exchange_subbands(sb, level, group)
+        if not overlap:
+            for r in reqs:
+                r.wait()
+            reqs = []
+        self._run_inverse_band(band_inverse, sb, level, interior, out)
+        for r in reqs:
+            r.wait()
+        for e in edges:
+            self._run_inverse_band(band_inverse, sb, level, e, out)
+
     def allocate(self, new_empty, level: int = 0):
         """Buffer for level ``level``: ``new_empty(shape)`` -> tensor."""
         L = self.layout(level)

@@ -89,6 +89,57 @@ def test_row_strips_bitwise_equal_single_process(world, wavelet, levels, overlap
     assert all(results[r] for r in range(world)), results
 
 
+def _oracle_band_inverse(inv_prog):
+    def band_inverse(band, band_row0, height, r0, r1, out):
+        img = oracle.inverse([b.contiguous().numpy() for b in band], inv_prog, threads=1)
+        out.copy_(torch.from_numpy(img[2 * (r0 - band_row0):2 * (r1 - band_row0)]))
+    return band_inverse
+
+
+def _inverse_worker(rank, world, port, wavelet, overlap, h, w, q):
+    from paper_1705_08266_b200 import invert_scheme
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        scheme = build_scheme("non-separable-split", PLANS[wavelet])
+        fwd, inv = compile_scheme(scheme), compile_scheme(invert_scheme(scheme))
+        img = np.random.default_rng(9).random((h, w)).astype(np.float32)
+        comps = oracle.forward(img, fwd)
+        want = oracle.inverse(comps, inv)
+        strips = RowStrips(h, w, rank, world, CONES[wavelet], levels=1)
+        sb = strips.allocate_subbands(lambda s: torch.zeros(s, dtype=torch.float32))
+        L = strips.layout(0)
+        a, b = L.row0 // 2, (L.row0 + L.rows) // 2
+        own = strips.owned_subbands(sb)
+        for c in range(4):
+            own[c].copy_(torch.from_numpy(comps[c][a:b]))
+        out = torch.zeros((L.rows, w), dtype=torch.float32)
+        strips.inverse(_oracle_band_inverse(inv), sb, out, overlap=overlap)
+        q.put((rank, bool(np.array_equal(out.numpy(), want[L.row0:L.row0 + L.rows]))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,wavelet,overlap,h,w", [
+    (2, "cdf97", True, 64, 40),
+    (4, "cdf53", False, 96, 36),
+    (4, "cdf97", True, 160, 36),
+])
+def test_inverse_row_strips_bitwise_equal_single_process(world, wavelet, overlap, h, w):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_inverse_worker, args=(r, world, port, wavelet, overlap, h, w, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(results[r] for r in range(world)), results
+
+
 def test_shard_range_partitions():
     for n in (0, 1, 7, 1024):
         for world in (1, 2, 3, 8):
