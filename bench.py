@@ -15,6 +15,8 @@ transforms its own image: batch sharding, no data-path collective ("weak").
 --config c5 : BASELINE configs[4], one 65536^2 image, non-separable CDF 9/7,
               1 level, row strips over N GPUs with an NCCL halo exchange.
 --config c2 : 4096^2, one line per scheme x wavelet x direction (parity sizes).
+--config c1 : BASELINE configs[0], 1024^2 9/7 separable lifting, 1 level: device
+              kernel, host-array call end to end, and the CPU oracle on the same image.
 
 --impl reference times the reference algorithm's CPU implementation on this
 box's host cores (the oracle port, oracle/dwt_oracle.c -- the reference itself
@@ -128,6 +130,10 @@ def _cpu_sample(config, steps=1, warmup=0):
         n, levels, scheme = 2048, 1, "non-separable-split"
         desc = "2 of the 1024 C4 images (2048x2048 f32), CDF 9/7 non-separable-split, 1 level"
         px = 2 * n * n
+    elif config == "c1":
+        n, levels, scheme = 1024, 1, "separable-lifting"
+        desc = "the whole C1 image (1024x1024 f32), CDF 9/7 separable-lifting, 1 level"
+        px = n * n
     elif config == "c5":
         n, levels, scheme = 8192, 1, "non-separable-split"
         desc = "one 8192x8192 f32 block (1/64 of the C5 area), CDF 9/7 non-separable-split, 1 level"
@@ -191,6 +197,7 @@ def _workload_name(config):
         "c4": "C4: 1024 x 2048x2048 f32, CDF 9/7 non-separable-split forward, 1 level, batch-sharded",
         "c5": "C5: 65536x65536 f32, CDF 9/7 non-separable-split forward, 1 level, row strips + NCCL halo exchange",
         "c2": "C2: 4096x4096 f32, all schemes x CDF 5/3, 9/7 x fwd/inv, 1 level",
+        "c1": "C1: 1024x1024 f32, CDF 9/7 separable-lifting forward, 1 level (the reference's CPU-runnable case)",
     }[config]
 
 
@@ -517,6 +524,57 @@ def run_c5(args):
     return 0
 
 
+def run_c1(args):
+    """C1 on one GPU: the device kernel (CUDA graph of K forwards, L2-warm: the
+    1024^2 image is 4 MiB), the reference-shaped host call end to end, and the
+    CPU oracle on the same image."""
+    import numpy as np
+    import torch
+
+    from paper_1705_08266_b200 import CDF97, Image2D, Transform, build_scheme, forward
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    n = 1024
+    scheme = build_scheme("separable-lifting", CDF97)
+    tr = Transform(scheme, "single", fast=(args.arith == "fast"))
+    img = Image2D.random(n, n, seed=0, precision="single")
+    x = torch.from_numpy(img.data).cuda()
+    out = tr.forward(x)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        tr.forward(x, out=out)
+    with ClockSampler(0) as clk:
+        ms = _time_graph(torch, None, graph, args.steps, args.warmup)
+    value = n * n / (ms * 1e-3) / 1e9
+    for _ in range(2):
+        forward(img, scheme)
+    t0 = time.perf_counter()
+    reps = max(3, args.steps)
+    for _ in range(reps):
+        forward(img, scheme)
+    e2e_ms = (time.perf_counter() - t0) / reps * 1e3
+    peak, src = _peaks()
+    cpu = None
+    if not args.no_cpu:
+        gpx, desc, threads, _, _ = _cpu_sample("c1", steps=3, warmup=1)
+        cpu = {"value": gpx, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (Image2D.random, PCG64 seed 0)",
+        "config": {"workload": _workload_name("c1"), "arith": args.arith,
+                   "l2": "4 MiB image: L2-resident (warm), a latency-bound launch"},
+        "roofline": {"bound": "hbm", "achieved": 8.0 * n * n / (ms * 1e-3) / 1e9, "peak": peak, "peak_source": src,
+                     "unit": "GB/s", "frac": 8.0 * n * n / (ms * 1e-3) / 1e9 / peak, "traffic": None},
+        "cpu_baseline": cpu,
+        "e2e": {"value": n * n / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": n * n * 4,
+                "d2h_bytes_per_step": n * n * 4, "ms_per_step": e2e_ms,
+                "api": "paper_1705_08266_b200.forward(Image2D, scheme) (NumPy in, NumPy out), wall clock"},
+        "clocks": clk.summary(), "gpu_launches": args.steps,
+    }), flush=True)
+    return 0
+
+
 def run_c2(args):
     import torch
 
@@ -557,7 +615,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("c3", "c4", "c5", "c2"), default="c3")
+    ap.add_argument("--config", choices=("c3", "c4", "c5", "c2", "c1"), default="c3")
     ap.add_argument("--arith", choices=("strict", "fast"), default="fast",
                     help="fast: FMA within the north-star tolerance (default); strict: bit-exact")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
@@ -565,7 +623,7 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
-    return {"c3": run_c3, "c4": run_c4, "c5": run_c5, "c2": run_c2}[args.config](args)
+    return {"c3": run_c3, "c4": run_c4, "c5": run_c5, "c2": run_c2, "c1": run_c1}[args.config](args)
 
 
 if __name__ == "__main__":
