@@ -23,6 +23,7 @@ from .engine import (
     inverse,
     run_reference,
     run_tiled,
+    run_without_barriers,
 )
 from .lifting import (
     CDF53,

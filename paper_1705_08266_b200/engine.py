@@ -53,6 +53,7 @@ __all__ = [
     "idwt",
     "run_tiled",
     "run_reference",
+    "run_without_barriers",
     "deinterleave",
     "interleave_quad",
 ]
@@ -695,6 +696,50 @@ def run_tiled(program, comps, cfg: TileConfig) -> list:
         "run_tiled",
     )
     return [_to_host(o) for o in out]
+
+
+def run_without_barriers(program, comps, cfg: TileConfig) -> list:
+    """Fault model: the inter-pass barriers dropped (engine.py:454-475).
+
+    Tiles run one after another, each taking the whole program to completion
+    in place on the shared state, so later tiles read a mix of fresh and stale
+    neighbours -- the race a barrier prevents, made deterministic as a
+    regression witness.  On the GPU: per (tile, sub-step), the sub-step is
+    evaluated over the current state (reflection at the image edges, as the
+    reference) and only the tile's window is written back.  Bit-identical to
+    the reference's fault model (tests/golden/nobarrier.npz).
+    """
+    from .program import PassProgram, StencilProgram
+
+    torch = _require_cuda()
+    dtype = np.dtype(comps[0].dtype)
+    if dtype not in _NP2NATIVE:
+        raise TypeError("components must be float32 or float64")
+    rows, cols = comps[0].shape
+    state = [_to_device(torch, np.ascontiguousarray(c)).clone() for c in comps]
+    scratch = [torch.empty_like(c) for c in state]
+    subs = [sub for p in program.passes for sub in p.substeps]
+    plans = [plan_for(StencilProgram(program.scheme_name if hasattr(program, "scheme_name") else "custom",
+                                     getattr(program, "wavelet", "custom"),
+                                     (PassProgram(f"sub{i}", "lift", True, (sub,)),)),
+                      _NP2NATIVE[dtype], _native.NO_TILE)
+             for i, sub in enumerate(subs)]
+    if cfg.tile is None:
+        tiles = [(0, rows, 0, cols)]
+    else:
+        tw, th = cfg.tile
+        tiles = [(r, min(r + th, rows), c, min(c + tw, cols)) for r in range(0, rows, th) for c in range(0, cols, tw)]
+    lib = _native.load()
+    pin = _native.planes([_ptr(c) for c in state], [c.stride(0) for c in state], 0)
+    pout = _native.planes([_ptr(c) for c in scratch], [c.stride(0) for c in scratch], 0)
+    stream = _stream_handle(torch, None)
+    for r0, r1, c0, c1 in tiles:
+        for plan in plans:
+            _native.check(lib.b2dwt_run_components(plan.handle, pin, pout, rows, cols, 1, stream),
+                          "run_without_barriers")
+            for t in range(4):
+                state[t][r0:r1, c0:c1] = scratch[t][r0:r1, c0:c1]
+    return [_to_host(c) for c in state]
 
 
 def run_reference(program, comps) -> list:

@@ -129,3 +129,29 @@ def test_impulse_response_matches_transfer_matrix():
 def test_subband_shape_errors():
     with pytest.raises(ValueError, match="all four subbands must share dimensions"):
         SubbandQuad(*(Image2D(np.zeros(s)) for s in ((2, 2), (2, 2), (2, 2), (2, 4))))
+
+
+def test_missing_barrier_witness_matches_reference_fault_model():
+    """run_without_barriers (engine.py:454-475): the barrier-free fault model is
+    bit-identical to the reference's, corrupts tiled runs, and is harmless
+    with one tile (tests/test_engine.py:241-259 witnesses)."""
+    import os
+
+    from paper_1705_08266_b200 import Image2D as I2, run_without_barriers
+
+    gold = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "nobarrier.npz"))
+    comps = deinterleave(I2.random(64, 48, seed=21))
+    for wname, plan in PLANS.items():
+        for scheme in ("separable-lifting", "non-separable-split"):
+            prog = compile_scheme(build_scheme(scheme, plan))
+            good = run_reference(prog, comps)
+            for tile in ((8, 8), (16, 4), None):
+                key = f"{wname}/{scheme}/{'full' if tile is None else f'{tile[0]}x{tile[1]}'}"
+                got = run_without_barriers(prog, comps, TileConfig(tile=tile))
+                for c, name in enumerate(("ll", "hl", "lh", "hh")):
+                    assert np.array_equal(got[c], gold[f"{key}/{name}"]), (key, name)
+                worst = max(float(np.abs(g - b).max()) for g, b in zip(good, got))
+                if tile is None:
+                    assert worst == 0.0, key
+                else:
+                    assert worst > 1e-6, key
