@@ -387,15 +387,18 @@ cudaError_t launch_gtile(const b2dwt_plan_s& p, const GTileProgram& g, const Fus
   if (e != cudaSuccess) return e;
   e = cudaMemcpyAsync(dg, &g, sizeof(GTileProgram), cudaMemcpyHostToDevice, r.stream);
   if (e == cudaSuccess) {
+    // opt in to the large dynamic shared memory once per instantiation
+    static const cudaError_t attr_strict = cudaFuncSetAttribute(
+        generic_tile_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    static const cudaError_t attr_fast = cudaFuncSetAttribute(
+        generic_tile_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (strict_of(&p)) {
-      e = cudaFuncSetAttribute(generic_tile_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem));
+      e = attr_strict;
       if (e == cudaSuccess)
         generic_tile_kernel<T, true><<<static_cast<unsigned>(n), kGTileThreads, smem, r.stream>>>(
             a, static_cast<const GTileProgram*>(dg));
     } else {
-      e = cudaFuncSetAttribute(generic_tile_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem));
+      e = attr_fast;
       if (e == cudaSuccess)
         generic_tile_kernel<T, false><<<static_cast<unsigned>(n), kGTileThreads, smem, r.stream>>>(
             a, static_cast<const GTileProgram*>(dg));

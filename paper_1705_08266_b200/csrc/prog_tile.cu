@@ -70,7 +70,13 @@ cudaError_t launch_tile(const FusedLaunch& r) {
   using TG = TileGeo<P, 32>;
   const int64_t tiles = static_cast<int64_t>(r.batch) * ((r.rows + TG::kTR - 1) / TG::kTR) *
                         ((r.cols + TG::kTC - 1) / TG::kTC);
-  const int wr = r.tile_rows > 0 ? r.tile_rows : (tiles >= 2 * 148 ? 32 : 16);
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      n = 148;
+    return n;
+  }();
+  const int wr = r.tile_rows > 0 ? r.tile_rows : (tiles >= 2 * sms ? 32 : 16);
   // f64 keeps to 16 rows: its 32-row load phase would spill
   if constexpr (sizeof(T) == 4) {
     if (wr >= 32) return launch_tile_wr<P, T, kStrict, 32>(r);
