@@ -390,10 +390,14 @@ class Transform:
 
     # multi level -----------------------------------------------------------------------
     def dwt(self, x, levels: int, stream=None):
-        """Return (ll, [(hl, lh, hh) per level, finest first])."""
+        """Return (ll, [(hl, lh, hh) per level, finest first]).  ``x`` is one
+        ``[H, W]`` image or a ``[B, H, W]`` batch (every level then runs as one
+        batched launch sequence; outputs gain the leading batch dimension)."""
         torch = self._check(x, "x")
+        if x.dim() == 3:
+            return self._dwt_batch(x, levels, stream)
         if x.dim() != 2:
-            raise ValueError("dwt takes one [H, W] image")
+            raise ValueError("dwt takes one [H, W] image or a [B, H, W] batch")
         h, w = x.shape
         if levels < 1:
             raise ValueError("levels must be >= 1")
@@ -408,6 +412,32 @@ class Transform:
             if levels > 1 else None
         self.dwt_into(x, levels, details, ll, scratch, stream)
         return ll, details
+
+    def _dwt_batch(self, x, levels, stream=None):
+        torch = _torch()
+        b, h, w = x.shape
+        if levels < 1:
+            raise ValueError("levels must be >= 1")
+        if h % (1 << levels) or w % (1 << levels):
+            raise ValueError(f"dimensions must be divisible by 2^{levels}, got {w}x{h}")
+        details, src = [], x
+        for lvl in range(levels):
+            shp = (b, h >> (lvl + 1), w >> (lvl + 1))
+            ll = torch.empty(shp, dtype=x.dtype, device=x.device)
+            bands = tuple(torch.empty(shp, dtype=x.dtype, device=x.device) for _ in range(3))
+            self.forward(src, out=(ll,) + bands, stream=stream)
+            details.append(bands)
+            src = ll
+        return src, details
+
+    def _idwt_batch(self, ll, details, out=None, stream=None):
+        torch = _torch()
+        cur = ll
+        for lvl in range(len(details) - 1, -1, -1):
+            hl, lh, hh = details[lvl]
+            dst = out if lvl == 0 and out is not None else None
+            cur = self.inverse(cur, hl, lh, hh, out=dst, stream=stream)
+        return cur
 
     def dwt_into(self, x, levels, details, ll, scratch, stream=None):
         torch = _torch()
@@ -483,6 +513,8 @@ class Transform:
 
     def idwt(self, ll, details, out=None, stream=None):
         torch = self._check(ll, "ll")
+        if ll.dim() == 3:
+            return self._idwt_batch(ll, details, out, stream)
         levels = len(details)
         h, w = ll.shape[0] << levels, ll.shape[1] << levels
         if out is None:

@@ -344,3 +344,19 @@ def test_inverse_rows_band_equals_full():
         band = tuple(c[b0:b1].contiguous() for c in q)
         got = tr.inverse_rows(band, b0, 512, r0, r1)
         assert torch.equal(got, full[2 * r0:2 * r1]), (r0, r1)
+
+
+def test_batched_pyramid_equals_items():
+    tr = _golden_transform("cdf97", "non-separable-split", "single")
+    x = torch.rand((5, 256, 384), device="cuda")
+    ll, det = tr.dwt(x, 4)
+    assert ll.shape == (5, 16, 24)
+    for b in range(5):
+        lb, db = tr.dwt(x[b].contiguous(), 4)
+        assert torch.equal(ll[b], lb)
+        for lvl in range(4):
+            for u, v in zip(det[lvl], db[lvl]):
+                assert torch.equal(u[b], v), (b, lvl)
+    rec = tr.idwt(ll, det)
+    for b in range(5):
+        assert torch.equal(rec[b], tr.idwt(ll[b].contiguous(), [tuple(t[b].contiguous() for t in d) for d in det]))
