@@ -15,7 +15,6 @@ import numpy as np
 import pytest
 
 from oracle import oracle
-from tests import golden_data as G
 
 pytestmark = pytest.mark.gpu
 
@@ -23,7 +22,7 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():  # pragma: no cover - CPU container
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from paper_1705_08266_b200 import CDF97, Transform, build_scheme, compile_scheme, invert_scheme  # noqa: E402
+from paper_1705_08266_b200 import CDF97, Transform, build_scheme, compile_scheme  # noqa: E402
 
 SCHEME = build_scheme("non-separable-split", CDF97)
 

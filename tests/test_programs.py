@@ -2,7 +2,6 @@
 compiled StencilPrograms bit for bit, and the generated kernel structures are
 current."""
 
-import numpy as np
 import pytest
 
 from paper_1705_08266_b200 import CDF53, CDF97, SCHEME_NAMES, build_scheme, compile_scheme, get_plan, invert_scheme
