@@ -16,12 +16,20 @@
  *   b2dwt_forward_rows    <- forward() restricted to a band of output rows of a
  *                            larger image (multi-GPU row strips; new, no reference
  *                            counterpart; reflection stays in global coordinates)
+ *   b2dwt_inverse_rows    <- inverse() restricted to a band of output rows (new)
  *   b2dwt_dwt / b2dwt_idwt<- multi-level pyramid (new; oracle = forward iterated
  *                            on ll)
+ *   b2dwt_dwt_host /      <- the same pyramids from / to HOST arrays, as the
+ *   b2dwt_idwt_host          reference's callers hold them (engine.py:481-495);
+ *                            PCIe copies pipelined in row bands
+ *   b2dwt_lift1d /        <- apply_plan_1d / invert_plan_1d, schemes.py:806-856
+ *   b2dwt_unlift1d           (batched 1-D lifting)
  *
  * Conventions
- *   - All pixel pointers are DEVICE pointers owned by the caller; element type
- *     is float (B2DWT_F32) or double (B2DWT_F64) as given at plan creation.
+ *   - All pixel pointers are DEVICE pointers owned by the caller (except the
+ *     image / subband pointers of b2dwt_dwt_host and b2dwt_idwt_host, which
+ *     are host pointers); element type is float (B2DWT_F32) or double
+ *     (B2DWT_F64) as given at plan creation.
  *   - Leading dimensions (ld) and batch strides are in ELEMENTS.
  *   - Quad grid: an H x W image has rows = H/2, cols = W/2 quads; component 0..3
  *     = (even row, even col)=LL, (even, odd)=HL, (odd, even)=LH, (odd, odd)=HH
