@@ -582,6 +582,56 @@ class Transform:
             (stream if stream is not None else torch.cuda.current_stream()).synchronize()
         return out
 
+    def forward_host_batch(self, x, out=None, chunk: int = 16, sync: bool = True):
+        """Single-level forward of a HOST batch ``[B, H, W]`` into HOST subbands
+        (LL, HL, LH, HH), each ``[B, H/2, W/2]``, streaming chunks of images: the
+        upload of chunk k+1, the kernel of chunk k and the download of chunk
+        k-1 run concurrently (two device slots, three streams).  Pinned host
+        memory gives the overlap.  Bit-identical to :meth:`forward`."""
+        torch = _require_cuda()
+        if isinstance(x, np.ndarray):
+            x = torch.from_numpy(np.ascontiguousarray(x))
+        if x.device.type != "cpu" or x.dim() != 3 or not x.is_contiguous():
+            raise ValueError("forward_host_batch takes a contiguous host [B, H, W] tensor")
+        if x.dtype != self.torch_dtype:
+            raise TypeError(f"expected {self.torch_dtype}, got {x.dtype}")
+        b, h, w = x.shape
+        if h % 2 or w % 2:
+            raise ValueError(f"dimensions must be even, got {w}x{h}")
+        if out is None:
+            out = tuple(torch.empty((b, h // 2, w // 2), dtype=x.dtype, pin_memory=x.is_pinned()) for _ in range(4))
+        chunk = max(1, min(chunk, b))
+        dev_in = [torch.empty((chunk, h, w), dtype=x.dtype, device="cuda") for _ in range(2)]
+        dev_out = [torch.empty((4, chunk, h // 2, w // 2), dtype=x.dtype, device="cuda") for _ in range(2)]
+        main = torch.cuda.current_stream()
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        s_in.wait_stream(main)
+        s_out.wait_stream(main)
+        freed = [None, None]  # event: slot's previous download finished
+        for k, i0 in enumerate(range(0, b, chunk)):
+            n = min(chunk, b - i0)
+            slot = k % 2
+            with torch.cuda.stream(s_in):
+                if freed[slot] is not None:
+                    s_in.wait_event(freed[slot])
+                dev_in[slot][:n].copy_(x[i0:i0 + n], non_blocking=True)
+                up = torch.cuda.Event()
+                up.record(s_in)
+            main.wait_event(up)
+            self.forward(dev_in[slot][:n], out=tuple(dev_out[slot][c, :n] for c in range(4)))
+            done = torch.cuda.Event()
+            done.record(main)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(done)
+                for c in range(4):  # contiguous slabs: one plain copy per plane
+                    out[c][i0:i0 + n].copy_(dev_out[slot][c, :n], non_blocking=True)
+                freed[slot] = torch.cuda.Event()
+                freed[slot].record(s_out)
+        main.wait_stream(s_out)  # later work on the caller's stream (and slot reuse) sees it all
+        if sync:
+            main.synchronize()
+        return out
+
     def inverse_rows(self, band, band_row0, global_height, out_row_begin, out_row_end, out=None, stream=None):
         """Image rows [2*out_row_begin, 2*out_row_end) of the inverse from a row
         band of the four subband planes (quad rows [band_row0, band_row0 +

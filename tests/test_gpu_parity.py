@@ -360,3 +360,15 @@ def test_batched_pyramid_equals_items():
     rec = tr.idwt(ll, det)
     for b in range(5):
         assert torch.equal(rec[b], tr.idwt(ll[b].contiguous(), [tuple(t[b].contiguous() for t in d) for d in det]))
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_forward_host_batch_equals_device(pinned):
+    tr = _golden_transform("cdf97", "non-separable-split", "single")
+    x = torch.rand((11, 130, 262))
+    if pinned:
+        x = x.pin_memory()
+    got = tr.forward_host_batch(x, chunk=4)
+    want = tr.forward(x.cuda())
+    for c in range(4):
+        assert torch.equal(got[c], want[c].cpu()), c
