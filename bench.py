@@ -525,6 +525,27 @@ def run_c5(args):
     ms = _max_over_ranks(torch, dist, s.elapsed_time(e)) / args.steps
     value = n * n / (ms * 1e-3) / 1e9
     interior, edges = strips._bands(0)
+    # end to end on a 16384 x 65536 sample per rank (4 GiB each way): pinned
+    # host rows in, pinned subbands out, through the banded host pipeline
+    del buf, own, outs
+    torch.cuda.empty_cache()
+    sh = 16384
+    host_in = torch.empty((sh, n), dtype=torch.float32).pin_memory()
+    host_in.uniform_()
+    det = [tuple(torch.empty((sh // 2, n // 2), dtype=torch.float32).pin_memory() for _ in range(3))]
+    host_ll = torch.empty((sh // 2, n // 2), dtype=torch.float32).pin_memory()
+    tr.dwt_host(host_in, 1, details=det, ll=host_ll, bands=args.bands, sync=True)
+    _barrier(torch, dist)
+    es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    es.record()
+    for _ in range(2):
+        tr.dwt_host(host_in, 1, details=det, ll=host_ll, bands=args.bands, sync=False)
+    ee.record()
+    ee.synchronize()
+    e2e_ms = _max_over_ranks(torch, dist, es.elapsed_time(ee)) / 2
+    e2e = {"value": sh * n * world / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": sh * n * 4,
+           "d2h_bytes_per_step": sh * n * 4, "ms_per_step": e2e_ms, "sample": f"{sh} x {n} rows per rank",
+           "api": "Transform.dwt_host(levels=1) (b2dwt_dwt_host) with pinned host buffers"}
     peak, src = _peaks()
     if rank == 0:
         achieved = 8.0 * L.rows * n / (ms * 1e-3) / 1e9
@@ -538,7 +559,7 @@ def run_c5(args):
                        "arith": args.arith},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": src, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None},
-            "cpu_baseline": None, "e2e": None, "clocks": clk.summary(),
+            "cpu_baseline": None, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": args.steps * (_launches(interior[1] - interior[0], n // 2) + len(edges)),
         }), flush=True)
     if dist is not None:
