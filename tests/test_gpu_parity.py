@@ -303,12 +303,14 @@ def test_footprint_split_launches_bit_exact(monkeypatch):
     whole = tr.forward(x)
     whole_b = tr.forward(xb)
     rec = tr.inverse(*whole)
+    rec_b = tr.inverse(*whole_b)
     monkeypatch.setenv("B2DWT_MAX_LAUNCH_BYTES", str(1 << 20))
     for a, b in zip(tr.forward(x), whole):
         assert torch.equal(a, b)
     for a, b in zip(tr.forward(xb), whole_b):
         assert torch.equal(a, b)
     assert torch.equal(tr.inverse(*whole), rec)
+    assert torch.equal(tr.inverse(*whole_b), rec_b)
 
 
 @pytest.mark.parametrize("shape,levels,bands,pinned", [
