@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges for nsys / ncu (no link dependency)
+
 #include "../../include/b2dwt.h"
 #include "generic_kernel.cuh"
 #include "generic_tile.cuh"
@@ -89,6 +91,19 @@ const Builtin* builtins() {
 
 // Error reporting for the other host units (host_pipeline.cu).
 int set_last_error(int code, const char* msg) { return fail(code, msg); }
+
+// NVTX ranges around pyramid levels and host-pipeline bands (nsys timelines),
+// only when B2DWT_NVTX is set so the default path makes no NVTX calls.
+bool nvtx_on() {
+  static const bool on = std::getenv("B2DWT_NVTX") != nullptr;
+  return on;
+}
+NvtxRange::NvtxRange(const char* name) : active(nvtx_on()) {
+  if (active) nvtxRangePushA(name);
+}
+NvtxRange::~NvtxRange() {
+  if (active) nvtxRangePop();
+}
 
 }  // namespace b2dwt
 
@@ -917,6 +932,9 @@ int b2dwt_dwt(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t heig
       lv.ptr[0] = sc[l & 1];
       lv.ld[0] = w / 2;
     }
+    char name[32];
+    std::snprintf(name, sizeof(name), "b2dwt dwt level %d", l);
+    NvtxRange range(name);
     if (int rc = b2dwt_forward(plan, in, in_ld, 0, h, w, &lv, 1, stream)) return rc;
     in = lv.ptr[0];
     in_ld = lv.ld[0];
@@ -953,6 +971,9 @@ int b2dwt_idwt(b2dwt_plan plan, const void* ll, int64_t ll_ld, const b2dwt_plane
     in.ptr[0] = const_cast<void*>(cur);
     in.ld[0] = cur_ld;
     in.bstride = 0;
+    char name[32];
+    std::snprintf(name, sizeof(name), "b2dwt idwt level %d", l);
+    NvtxRange range(name);
     if (int rc = b2dwt_inverse(plan, &in, dst, dst_ld, 0, h, w, 1, stream)) return rc;
     cur = dst;
     cur_ld = dst_ld;

@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "../../include/b2dwt.h"
+#include "launch.h"
 
 namespace b2dwt {
 int set_last_error(int code, const char* msg);  // b2dwt_host.cu: b2dwt_last_error() text
@@ -180,6 +181,9 @@ int b2dwt_dwt_host(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t
   // level-0 band, every band of a coarser level whose producer is enqueued
   auto emit = [&](int l, int k) -> int {
     cudaStream_t s_o = res.s_out;
+    char name[40];
+    std::snprintf(name, sizeof(name), "b2dwt dwt_host level %d band %d", l, k);
+    b2dwt::NvtxRange range(name);
     cudaEvent_t wait = l == 0 ? ev_in[deps[l][k]] : ev_band[l - 1][deps[l][k]];
     if ((e = cudaStreamWaitEvent(s_comp, wait, 0)) != cudaSuccess)
       return pipe_fail(B2DWT_ECUDA, std::string("wait: ") + cudaGetErrorString(e));

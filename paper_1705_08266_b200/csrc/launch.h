@@ -43,6 +43,15 @@ struct FusedLaunch {
   cudaStream_t stream;
 };
 
+// RAII NVTX range (b2dwt_host.cu); a no-op unless B2DWT_NVTX is set.
+struct NvtxRange {
+  explicit NvtxRange(const char* name);
+  ~NvtxRange();
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+  bool active;
+};
+
 // Cone of a built-in program (quads): halo the caller must provide.
 struct ConeInfo {
   int up, down, left, right;
