@@ -2,12 +2,15 @@
 """Benchmark: Gpixel/s of the 2-D CDF 9/7 forward DWT on B200 vs the HBM roofline.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c3|c4|c5|c2] [--arith strict|fast]
+                    [--config c3|c4|c5|c2|c1] [--arith strict|fast] [--bands K]
 
 Default workload (BASELINE.json configs[2], the north-star target, "C3"):
 one 16384x16384 float32 image, operation-reduced non-separable CDF 9/7
 ("non-separable-split") forward transform, 5-level pyramid, per GPU.  A step is
-one full pyramid (5 fused kernel launches).  Under torchrun (N > 1) every rank
+one replay of a CUDA graph holding the whole pyramid (6 launches: level 0 as
+two footprint-bounded row bands, levels 1-3 streamed, level 4 tiled).  `e2e`
+runs the same pyramid from pinned host memory to pinned host memory through
+Transform.dwt_host.  Under torchrun (N > 1) every rank
 transforms its own image: batch sharding, no data-path collective ("weak").
 
 --config c4 : BASELINE configs[3], 1024 x 2048^2 images, non-separable CDF 9/7,
