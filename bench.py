@@ -117,6 +117,62 @@ class ClockSampler:
 # -- CPU reference arm ----------------------------------------------------------------
 
 
+def _cpu_model():
+    """The host CPU model (lscpu's "Model name"), from /proc/cpuinfo."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _stock_reference_sample(config):
+    """The UNMODIFIED reference (liftfuse, pip-installed into the git-ignored
+    baseline/_ref) through its own timed region, liftfuse/bench.py:71-79:
+    run_tiled on pre-deinterleaved components, TileConfig((256, 256),
+    os.cpu_count()), median of 3 after one warm-up, iterated on LL for the
+    pyramid.  Bounded sample: a quarter-side crop of the workload image (C3:
+    4096^2, 5 levels).  Returns None when baseline/_ref is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "liftfuse")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        from liftfuse.engine import Image2D, TileConfig, compile_scheme, deinterleave, run_tiled
+        from liftfuse.schemes import build_scheme
+        from liftfuse.wavelets import CDF97
+    except Exception as exc:  # pragma: no cover - broken install
+        return {"unavailable": f"baseline/_ref import failed: {exc}"}
+    n, levels, scheme = {"c1": (1024, 1, "separable-lifting"), "c4": (2048, 1, "non-separable-split"),
+                         "c5": (4096, 1, "non-separable-split"), "c2": (4096, 1, "non-separable-split")}.get(
+        config, (4096, 5, "non-separable-split"))
+    threads = os.cpu_count() or 1
+    prog = compile_scheme(build_scheme(scheme, CDF97))
+    cfg = TileConfig((256, 256), threads)
+    comps0 = deinterleave(Image2D.random(n, n, seed=0, precision="single"))
+
+    def pyramid():  # seconds inside run_tiled
+        comps, spent = comps0, 0.0
+        for lvl in range(levels):
+            t0 = time.perf_counter()
+            out = run_tiled(prog, comps, cfg)
+            spent += time.perf_counter() - t0
+            if lvl + 1 < levels:
+                comps = deinterleave(Image2D(out[0]))
+        return spent
+
+    pyramid()  # warm-up, excluded
+    med = statistics.median(pyramid() for _ in range(3))
+    return {"value": n * n / med / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{n}x{n} f32, CDF 9/7 {scheme}, {levels} level(s): stock liftfuse run_tiled "
+                      f"(TileConfig((256,256), {threads})), deinterleave between levels excluded",
+            "ms_per_sample": med * 1e3}
+
+
 def _cpu_sample(config, steps=1, warmup=0):
     """Time the oracle port on a bounded sample; returns (gpx_per_s, sample_desc, threads, per_step_s)."""
     import numpy as np
@@ -126,8 +182,8 @@ def _cpu_sample(config, steps=1, warmup=0):
 
     threads = os.cpu_count() or 1
     if config == "c3":
-        n, levels, scheme = 8192, 5, "non-separable-split"
-        desc = "8192x8192 f32 (1/4 of the C3 area), CDF 9/7 non-separable-split, 5-level pyramid"
+        n, levels, scheme = 16384, 5, "non-separable-split"
+        desc = "the whole C3 workload: 16384x16384 f32, CDF 9/7 non-separable-split, 5-level pyramid"
         px = n * n
     elif config == "c4":
         n, levels, scheme = 2048, 1, "non-separable-split"
@@ -170,6 +226,7 @@ def run_reference(args):
         return 0
     steps = max(1, args.steps)
     gpx, desc, threads, med, times = _cpu_sample(args.config, steps=steps, warmup=min(args.warmup, 1))
+    stock = _stock_reference_sample(args.config)
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -184,11 +241,14 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (uniform [0,1), numpy PCG64 seed 0)",
-        "config": {"workload": _workload_name(args.config), "sample": desc},
-        "cpu_baseline": {"value": gpx, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc},
+        "config": {"workload": _workload_name(args.config), "sample": desc,
+                   "same_config": args.config != "c4"},
+        "cpu_baseline": {"value": gpx, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc,
+                         "cpu_model": _cpu_model(), "stock_reference": stock},
         "e2e": {"value": gpx, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "oracle/dwt_oracle.c: C restatement of liftfuse run_reference (bit-identical to the reference, "
-                "pinned by tests/test_oracle.py); the reference itself is pure Python/NumPy",
+        "note": "value: oracle/dwt_oracle.c, the C restatement of liftfuse run_reference (bit-identical to the "
+                "reference, pinned by tests/test_oracle.py), on all host threads; cpu_baseline.stock_reference: "
+                "the unmodified liftfuse package (baseline/_ref) on a bounded sample",
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -213,6 +273,12 @@ def _dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    if world > 1:
+        # NCCL communicator setup in the log (which transport / NVLS the box uses)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -254,6 +320,22 @@ def _launches(rows, cols, batch=1, levels=1):
     return total
 
 
+def _c3_launches(groups, n):
+    """Kernel launches of one C3 pyramid: a fused level pair runs as row bands of
+    <= 512 MiB of level-l input (b2dwt_host.cu run_fused2_pair), a single level
+    as _launches counts it."""
+    cap = int(os.environ.get("B2DWT_MAX_LAUNCH_BYTES", 512 << 20))
+    total = 0
+    for a, b in groups:
+        r = n >> (a + 1)
+        if a == b:
+            total += _launches(r, r, 1, 1)
+        else:
+            parts = -(-r * r * 16 // cap) if cap > 0 else 1
+            total += max(1, min(parts, (r // 2) // 128))
+    return total
+
+
 def _time_graph(torch, dist, graph, steps, warmup):
     """K replays between barrier + synchronize; returns ms per step (max over ranks)."""
     for _ in range(max(3, warmup)):
@@ -282,18 +364,21 @@ def run_c3(args):
     gen = torch.Generator(device="cuda")
     gen.manual_seed(rank)
     x = torch.rand((n, n), device="cuda", generator=gen)
-    # The product pyramid path: the whole 5-level pyramid is ONE CUDA graph
-    # (5 fused kernel launches chained by programmatic dependent launch, LL
-    # ping-pong in scratch, subbands into the pyramid).
+    # The product pyramid path: the whole 5-level pyramid is ONE CUDA graph of
+    # one b2dwt_dwt call (levels 0+1 and 2+3 as two-level fused kernels, whose
+    # LL bands never reach HBM, level 4 tiled; launches chained by
+    # programmatic dependent launch).
     graph = tr.capture_dwt(x, levels)
 
     with ClockSampler(local) as clk:
         ms_step = _time_graph(torch, dist, graph, args.steps, args.warmup)
     del graph
-    # level breakdown: the same pyramid captured with external event nodes
-    # bracketing every level (the events serialise the levels, so this graph
-    # is a little slower than the timed one), K replays, events read after each
+    # launch-group breakdown: the same pyramid captured with external event
+    # nodes bracketing every launch group (a fused level pair or a single
+    # level; the events serialise the groups, so this graph is a little slower
+    # than the timed one), K replays, events read after each
     ev_graph = tr.capture_dwt(x, levels, level_events=True)
+    groups = ev_graph.groups
     per_level_runs = []
     for _ in range(args.warmup + args.steps):
         ev_graph.replay()
@@ -301,7 +386,7 @@ def run_c3(args):
         per_level_runs.append(ev_graph.level_ms())
     per_level_runs = per_level_runs[args.warmup:]
     del ev_graph
-    per_level = [statistics.median(r[l] for r in per_level_runs) for l in range(levels)]
+    per_group = [statistics.median(r[g] for r in per_level_runs) for g in range(len(groups))]
     l0_ms = statistics.mean(r[0] for r in per_level_runs)
     # the other arithmetic mode, same protocol (reported beside the headline)
     other = Transform(scheme, "single", fast=not fast)
@@ -312,17 +397,34 @@ def run_c3(args):
     px = n * n * world
     value = px / (ms_step * 1e-3) / 1e9
     alg_bytes_step = 8 * n * n * sum(4.0 ** -l for l in range(levels))
-    l0_bytes = 8 * n * n
+    # dominant launch = the first group (levels 0+1 fused, or level 0 alone):
+    # SURVEY 8(d) algorithmic bytes = 1 read + 1 write of every level's input
+    # area it processes; the fused kernel's compulsory HBM bytes are smaller
+    # (level 0's LL band never leaves the SM): read the image, write level 0's
+    # HL/LH/HH and level 1's four planes
+    g0a, g0b = groups[0]
+    l0_bytes = 8 * n * n * sum(4.0 ** -l for l in range(g0a, g0b + 1))
+    l0_compulsory = 4 * n * n * (1 + 0.75 + (0.25 if g0b > g0a else 0.25))
     peak, peak_src = _peaks()
     achieved = l0_bytes / (l0_ms * 1e-3) / 1e9
 
     # end to end through the public API with host (pinned) buffers
     e2e = _e2e_c3(torch, tr, n, levels, rank, dist, args)
 
+    # at N > 1 the BASELINE scaling configs ride along: C4 (batch shards) and
+    # C5 (row strips + NCCL halo exchange), strong scaling, same ranks
+    scale_keys = {}
+    if world > 1 and not args.no_scale_configs:
+        torch.cuda.empty_cache()
+        scale_keys["c4"] = _measure_c4(args, torch, dist, world, rank, local, e2e_sample=False)
+        torch.cuda.empty_cache()
+        scale_keys["c5"] = _measure_c5(args, torch, dist, world, rank, local, e2e_sample=False)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         gpx, desc, threads, med, _ = _cpu_sample("c3")
-        cpu = {"value": gpx, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
+        cpu = {"value": gpx, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc,
+               "cpu_model": _cpu_model(), "stock_reference": _stock_reference_sample("c3")}
 
     strict_desc = "strict: bit-identical to the reference (separate IEEE mul/add, compiled term order)"
     fast_desc = "fast: FMA in the compiled term order, max err <= 1e-4 x input range (tests/test_gpu_parity.py)"
@@ -353,14 +455,18 @@ def run_c3(args):
                 "l2": "input 1 GiB > 126 MB L2 per step; no flush",
                 "parallelism": f"batch-shard x{world} (one image per GPU, no collective)",
                 "ns_per_px": 1.0 / value,
-                "ms_per_level": per_level,
+                "launch_groups": [f"L{a}" if a == b else f"L{a}+L{b} fused" for a, b in groups],
+                "ms_per_group": per_group,
                 "alg_bytes_per_step": alg_bytes_step,
                 "frac_of_8TBps": (alg_bytes_step / (ms_step * 1e-3) / 1e9) / SPEC_HBM_GBS,
             },
             "roofline": {
                 "bound": "hbm",
-                "kernel": "stream_kernel<cdf97_nssplit_fwd, f32> level 0 (16384^2 -> 4 x 8192^2; two "
-                          "footprint-bounded launches of 4096 quad rows, achieved/traffic per level)",
+                "kernel": ("fused2_kernel<cdf97_nssplit_fwd, f32>: levels 0+1 in one kernel (16384^2 -> "
+                           "HL/LH/HH 8192^2 + 4 x 4096^2; two footprint-bounded launches of 2048 level-1 rows)"
+                           if g0b > g0a else
+                           "stream_kernel<cdf97_nssplit_fwd, f32> level 0 (16384^2 -> 4 x 8192^2; two "
+                           "footprint-bounded launches of 4096 quad rows)"),
                 "achieved": achieved,
                 "peak": peak,
                 "peak_source": peak_src,
@@ -368,14 +474,18 @@ def run_c3(args):
                 "frac": achieved / peak,
                 "traffic": _traffic(f"c3_level0_{args.arith}"),
                 "alg_bytes_per_launch": l0_bytes,
+                "alg_bytes_rule": "SURVEY 8(d): 8 B/px of every level the launch processes",
+                "compulsory_bytes": l0_compulsory,
+                "frac_compulsory": l0_compulsory / (l0_ms * 1e-3) / 1e9 / peak,
                 "launch_ms": l0_ms,
-                "timing": "level-0 event nodes inside the captured graph, mean over K replays",
+                "timing": "event nodes around the first launch group inside the captured graph, mean over K replays",
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
-            "gpu_launches": args.steps * _launches(n // 2, n // 2, 1, levels),
+            "gpu_launches": args.steps * _c3_launches(groups, n),
         }
+        line.update(scale_keys)
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -420,6 +530,16 @@ def _e2e_c3(torch, tr, n, levels, rank, dist, args):
 
 def run_c4(args):
     torch, dist, world, rank, local = _dist_setup(args)
+    line = _measure_c4(args, torch, dist, world, rank, local, e2e_sample=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def _measure_c4(args, torch, dist, world, rank, local, e2e_sample=True):
+    """C4: 1024 x 2048^2 images batch-sharded over the ranks (no collective)."""
     from paper_1705_08266_b200 import CDF97, Transform, build_scheme
     from paper_1705_08266_b200.distributed import shard_range
 
@@ -456,6 +576,9 @@ def run_c4(args):
     # (Transform.forward_host_batch); 2 GiB each way per rank
     del x, outs
     torch.cuda.empty_cache()
+    if not e2e_sample:
+        return {"value": value, "unit": UNIT, "ms_per_step": ms, "scaling": "strong", "images_per_gpu": mine,
+                "roofline_frac": 8.0 * mine * n * n / (ms * 1e-3) / 1e9 / peak, "clocks": clk.summary()}
     sample = min(mine, 128)
     host_in = torch.empty((sample, n, n), dtype=torch.float32).pin_memory()
     host_in.uniform_()
@@ -473,9 +596,8 @@ def run_c4(args):
     e2e = {"value": sample * world * n * n / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": sample * n * n * 4, "d2h_bytes_per_step": sample * n * n * 4, "ms_per_step": e2e_ms,
            "sample": f"{sample} images per rank", "api": "Transform.forward_host_batch (pinned host batch in and out)"}
-    if rank == 0:
-        achieved = 8.0 * mine * n * n / (ms * 1e-3) / 1e9
-        print(json.dumps({
+    achieved = 8.0 * mine * n * n / (ms * 1e-3) / 1e9
+    return {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (uniform on device)",
@@ -486,14 +608,21 @@ def run_c4(args):
                          "frac": achieved / peak, "traffic": None},
             "cpu_baseline": None, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": args.steps * _launches(n // 2, n // 2, mine),
-        }), flush=True)
+        }
+
+
+def run_c5(args):
+    torch, dist, world, rank, local = _dist_setup(args)
+    line = _measure_c5(args, torch, dist, world, rank, local, e2e_sample=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
     return 0
 
 
-def run_c5(args):
-    torch, dist, world, rank, local = _dist_setup(args)
+def _measure_c5(args, torch, dist, world, rank, local, e2e_sample=True):
+    """C5: one 65536^2 image in row strips over the ranks, NCCL halo exchange."""
     from paper_1705_08266_b200 import CDF97, Transform, build_scheme
     from paper_1705_08266_b200.distributed import RowStrips
 
@@ -532,6 +661,11 @@ def run_c5(args):
     # host rows in, pinned subbands out, through the banded host pipeline
     del buf, own, outs
     torch.cuda.empty_cache()
+    peak, src = _peaks()
+    if not e2e_sample:
+        return {"value": value, "unit": UNIT, "ms_per_step": ms, "scaling": "strong",
+                "rows_per_gpu": L.rows, "halo_rows_per_side_px": [L.halo_top, L.halo_bot],
+                "roofline_frac": 8.0 * L.rows * n / (ms * 1e-3) / 1e9 / peak, "clocks": clk.summary()}
     sh = 16384
     host_in = torch.empty((sh, n), dtype=torch.float32).pin_memory()
     host_in.uniform_()
@@ -549,10 +683,8 @@ def run_c5(args):
     e2e = {"value": sh * n * world / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": sh * n * 4,
            "d2h_bytes_per_step": sh * n * 4, "ms_per_step": e2e_ms, "sample": f"{sh} x {n} rows per rank",
            "api": "Transform.dwt_host(levels=1) (b2dwt_dwt_host) with pinned host buffers"}
-    peak, src = _peaks()
-    if rank == 0:
-        achieved = 8.0 * L.rows * n / (ms * 1e-3) / 1e9
-        print(json.dumps({
+    achieved = 8.0 * L.rows * n / (ms * 1e-3) / 1e9
+    return {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (uniform on device)",
@@ -564,10 +696,7 @@ def run_c5(args):
                          "frac": achieved / peak, "traffic": None},
             "cpu_baseline": None, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": args.steps * (_launches(interior[1] - interior[0], n // 2) + len(edges)),
-        }), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
-    return 0
+        }
 
 
 def run_c1(args):
@@ -655,6 +784,19 @@ def run_c2(args):
     return 0
 
 
+def _spawn(args):
+    """`bench.py --gpus N` (N > 1) run directly: re-launch as N ranks, one per
+    GPU, exactly as the driver does (torch.distributed.run, 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -666,7 +808,11 @@ def main():
                     help="fast: FMA within the north-star tolerance (default); strict: bit-exact")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--bands", type=int, default=16, help="row bands of the host-buffer (e2e) pipeline")
+    ap.add_argument("--no-scale-configs", action="store_true",
+                    help="N > 1: skip the C4 / C5 strong-scaling keys of the default (C3) line")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _spawn(args)
     if args.impl == "reference":
         return run_reference(args)
     return {"c3": run_c3, "c4": run_c4, "c5": run_c5, "c2": run_c2, "c1": run_c1}[args.config](args)

@@ -19,6 +19,7 @@
  *   b2dwt_inverse_rows    <- inverse() restricted to a band of output rows (new)
  *   b2dwt_dwt / b2dwt_idwt<- multi-level pyramid (new; oracle = forward iterated
  *                            on ll)
+ *   b2dwt_forward2        <- two levels of that pyramid in one kernel (new)
  *   b2dwt_dwt_host /      <- the same pyramids from / to HOST arrays, as the
  *   b2dwt_idwt_host          reference's callers hold them (engine.py:481-495);
  *                            PCIe copies pipelined in row bands
@@ -72,7 +73,9 @@ enum {
     B2DWT_FORCE_GENERIC = 4, /* use the per-sub-step interpreter kernel (debug)      */
     B2DWT_NO_TMA = 8,        /* fused kernel loads with cp.async instead of TMA      */
     B2DWT_NO_TILE = 16,      /* never use the 2-D tile kernel (small levels stream)  */
-    B2DWT_FORCE_TILE = 32    /* tile kernel for every whole-image level it supports  */
+    B2DWT_FORCE_TILE = 32,   /* tile kernel for every whole-image level it supports  */
+    B2DWT_NO_FUSE = 64       /* b2dwt_dwt: one launch per level (no two-level fused
+                                kernel; results are identical either way)           */
 };
 
 /* One multiply-accumulate term: out[target][n,m] += coeff * in[src][n+dn, m+dm] */
@@ -165,6 +168,18 @@ int b2dwt_inverse_rows(b2dwt_plan plan, const b2dwt_planes* in, int64_t in_row0,
 int b2dwt_dwt(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t height, int64_t width,
               int32_t levels, const b2dwt_planes* details, void* ll_out, int64_t ll_ld, void* scratch,
               void* stream);
+
+/* Two pyramid levels in ONE kernel (new): level 0 of the height x width
+ * `image` and level 1 of its LL, which never leaves the SM (the LL band of
+ * level 0 is not written anywhere).  det0.ptr[1..3] receive level 0's HL/LH/HH
+ * ((H/2) x (W/2)), out1.ptr[0..3] level 1's LL/HL/LH/HH ((H/4) x (W/4)).
+ * Bit-identical to two b2dwt_forward calls.  Returns B2DWT_EUNSUPPORTED when
+ * the plan or geometry does not fit the fused kernel (built-in forward lifting
+ * program, f32, 16-B aligned image pitch, W >= 256, H and W divisible by 4, no
+ * B2DWT_NO_FUSE / NO_TMA / FORCE_GENERIC flag); the caller then runs two
+ * levels.  b2dwt_dwt pairs its levels this way automatically. */
+int b2dwt_forward2(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t height, int64_t width,
+                   const b2dwt_planes* det0, const b2dwt_planes* out1, void* stream);
 
 /* Multi-level inverse: `plan` holds the inverse program.  Reconstructs the
  * height x width image from ll (of the coarsest level) and details[l].

@@ -12,14 +12,16 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libb2dwt.so")
+# B2DWT_LIB: another in-tree build of the same library (development
+# experiments, e.g. tools/ variants built with extra -D flags)
+LIB_PATH = os.environ.get("B2DWT_LIB") or os.path.join(HERE, "libb2dwt.so")
 
 B2DWT_OK = 0
 B2DWT_EINVAL = -22
 B2DWT_EUNSUPPORTED = -95
 B2DWT_ECUDA = -5
 F32, F64 = 0, 1
-STRICT, FAST, FORCE_GENERIC, NO_TMA, NO_TILE, FORCE_TILE = 1, 2, 4, 8, 16, 32
+STRICT, FAST, FORCE_GENERIC, NO_TMA, NO_TILE, FORCE_TILE, NO_FUSE = 1, 2, 4, 8, 16, 32, 64
 
 # Every symbol include/b2dwt.h declares (tests check the .so exports all of them).
 EXPORTS = (
@@ -34,6 +36,7 @@ EXPORTS = (
     "b2dwt_inverse",
     "b2dwt_forward_rows",
     "b2dwt_dwt",
+    "b2dwt_forward2",
     "b2dwt_idwt",
     "b2dwt_dwt_host_workspace",
     "b2dwt_dwt_host",
@@ -126,6 +129,7 @@ def load():
             "b2dwt_inverse": (ctypes.c_int, [vp, P(Planes), vp, i64, i64, i64, i64, i32, vp]),
             "b2dwt_forward_rows": (ctypes.c_int, [vp, vp, i64, i64, i64, i64, i64, i64, i64, P(Planes), vp]),
             "b2dwt_dwt": (ctypes.c_int, [vp, vp, i64, i64, i64, i32, P(Planes), vp, i64, vp, vp]),
+            "b2dwt_forward2": (ctypes.c_int, [vp, vp, i64, i64, i64, P(Planes), P(Planes), vp]),
             "b2dwt_idwt": (ctypes.c_int, [vp, vp, i64, P(Planes), i32, vp, i64, i64, i64, vp, vp]),
             "b2dwt_dwt_host_workspace": (i64, [vp, i64, i64, i32]),
             "b2dwt_dwt_host": (ctypes.c_int, [vp, vp, i64, i64, i64, i32, P(Planes), vp, i64, vp, i64, i32, vp]),

@@ -8,6 +8,8 @@ Translation units:
   csrc/prog_variant.cu      ONE fused kernel per unit (program x element type x
                             layout x arithmetic x fill), compiled in parallel
   csrc/prog_tile.cu         per built-in program: the small-level tile kernels
+  csrc/prog_fused2.cu       per forward lifting program: two pyramid levels in one
+                            kernel (fused2_kernel.cuh), strict + fast
 
 Flags: -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 (ptxas -v output is
 kept in build/ptxas_<unit>.log for register / spill review).
@@ -112,6 +114,12 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
         defs = [f"-DB2DWT_PROG={ident}", f"-DB2DWT_PROG_INV={int(inv)}"]
         tasks.append((os.path.join(CSRC, "prog_dispatch.cu"), os.path.join(BUILD, f"dispatch_{ident}.o"),
                       ["-std=c++20", *defs], os.path.join(BUILD, f"ptxas_dispatch_{ident}.log")))
+        # two-level fused kernel: forward lifting programs (per-sub-step
+        # horizontal reach <= 1); a stub elsewhere
+        f2 = not inv and ident != "cdf97_conv_fwd" and (only is None or ident in only)
+        tasks.append((os.path.join(CSRC, "prog_fused2.cu"), os.path.join(BUILD, f"fused2_{ident}{'' if f2 else '_stub'}.o"),
+                      ["-std=c++20", *defs] + ([] if f2 else ["-DB2DWT_STUB"]),
+                      os.path.join(BUILD, f"ptxas_fused2_{ident}{'' if f2 else '_stub'}.log")))
         tag = "" if (only is None or ident in only) else "_stub"
         tasks.append((os.path.join(CSRC, "prog_tile.cu"), os.path.join(BUILD, f"tile_{ident}{tag}.o"),
                       ["-std=c++20", *defs] + (["-DB2DWT_STUB"] if tag else []),

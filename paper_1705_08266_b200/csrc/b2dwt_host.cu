@@ -16,6 +16,8 @@
 #include <mutex>
 #include <cstring>
 #include <string>
+#include <unordered_map>
+#include <utility>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges for nsys / ncu (no link dependency)
@@ -30,6 +32,7 @@ namespace b2dwt {
 #define B2DWT_DECLARE(ID, NAME)                                     \
   cudaError_t b2dwt_fused_##NAME(const FusedLaunch&, bool* used_tma); \
   cudaError_t b2dwt_tile_##NAME(const FusedLaunch&);                  \
+  cudaError_t b2dwt_fused2_##NAME(const Fused2Launch&);               \
   ConeInfo b2dwt_cone_##NAME();
 B2DWT_FOR_EACH_PROGRAM(B2DWT_DECLARE)
 #undef B2DWT_DECLARE
@@ -60,6 +63,7 @@ struct Builtin {
   TileLauncher tile;
   ConeGetter cone;
   bool inverse;
+  Fused2Launcher fused2;
 };
 
 template <class P>
@@ -80,7 +84,7 @@ const Builtin* builtins() {
 #define B2DWT_ROW(ID, NAME)                                                                                      \
   {progs::NAME::kKey,        progs::NAME::kNumSub, progs::NAME::kNumTerms, &begin_of<progs::NAME>,             \
    &term_of<progs::NAME>,    &coef_of<progs::NAME>,    &b2dwt_fused_##NAME,  &b2dwt_tile_##NAME, &b2dwt_cone_##NAME,     std::strstr(progs::NAME::kKey, "/inv") \
-   != nullptr},
+   != nullptr, &b2dwt_fused2_##NAME},
       B2DWT_FOR_EACH_PROGRAM(B2DWT_ROW)
 #undef B2DWT_ROW
   };
@@ -125,28 +129,68 @@ namespace {
 
 bool strict_of(const b2dwt_plan_s* p) { return (p->flags & B2DWT_FAST) == 0; }
 
-// Pool of zero-initialised {tickets, done} counter pairs per device for the
-// dynamic work tail.  Each launch takes the next slot round-robin; the kernel's
-// last warp resets its slot, so launches queued on one stream reuse slots
-// safely and up to kSlots launches may run concurrently on other streams.
-unsigned long long* tail_counter_slot() {
-  constexpr int kSlots = 256, kMaxDev = 64;
+// Zero-initialised {tickets, done} counter pairs for the dynamic work tail.
+// The kernel's last CTA resets its pair, so launches ordered on ONE stream can
+// share pairs safely; launches that may run concurrently must not.  Hence:
+//   * eager launches draw round-robin from a pool owned by their stream;
+//   * launches recorded into a CUDA graph draw from a capture arena whose pairs
+//     are never handed out again (a graph may replay concurrently with anything).
+// Pools are allocated and zeroed synchronously the first time a device is used
+// outside a capture; inside a capture with no arena left the launch runs a fully
+// static split (tail counter null), which is slower but exact.
+namespace {
+constexpr int kStreamSlots = 64;
+constexpr int kArenaSlots = 4096;
+struct DeviceCounters {
+  std::unordered_map<cudaStream_t, std::pair<unsigned long long*, unsigned>> streams;
+  unsigned long long* arena = nullptr;
+  int arena_used = 0;
+};
+unsigned long long* zeroed_pairs(int n) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, static_cast<size_t>(n) * 2 * sizeof(unsigned long long)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  // synchronous zeroing, complete before any stream can use the pairs
+  if (cudaMemset(p, 0, static_cast<size_t>(n) * 2 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
+    (void)cudaGetLastError();
+    cudaFree(p);
+    return nullptr;
+  }
+  return static_cast<unsigned long long*>(p);
+}
+}  // namespace
+
+unsigned long long* tail_counter_slot(cudaStream_t stream) {
+  constexpr int kMaxDev = 64;
   static std::mutex mu;
-  static unsigned long long* pool[kMaxDev] = {};
-  static unsigned next[kMaxDev] = {};
+  static DeviceCounters dev_counters[kMaxDev];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  if (!pool[dev]) {
-    void* p = nullptr;
-    if (cudaMalloc(&p, kSlots * 2 * sizeof(unsigned long long)) != cudaSuccess) {
-      (void)cudaGetLastError();
-      return nullptr;
-    }
-    cudaMemset(p, 0, kSlots * 2 * sizeof(unsigned long long));
-    pool[dev] = static_cast<unsigned long long*>(p);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
   }
-  return pool[dev] + 2 * (next[dev]++ % kSlots);
+  std::lock_guard<std::mutex> lock(mu);
+  DeviceCounters& d = dev_counters[dev];
+  if (cap != cudaStreamCaptureStatusNone) {
+    if (!d.arena || d.arena_used >= kArenaSlots) return nullptr;  // no allocation inside a capture
+    return d.arena + 2 * (d.arena_used++);
+  }
+  if (!d.arena || d.arena_used >= kArenaSlots) {  // (re)fill the capture arena while we may allocate
+    d.arena = zeroed_pairs(kArenaSlots);
+    d.arena_used = 0;
+  }
+  auto it = d.streams.find(stream);
+  if (it == d.streams.end()) {
+    unsigned long long* p = zeroed_pairs(kStreamSlots);
+    if (!p) return nullptr;
+    it = d.streams.emplace(stream, std::make_pair(p, 0u)).first;
+  }
+  return it->second.first + 2 * (it->second.second++ % kStreamSlots);
 }
 
 // Lower bound on rows per CTA (B2DWT_MIN_ROWS overrides).
@@ -482,7 +526,7 @@ int run_fused(const b2dwt_plan_s& p, FusedLaunch& r) {
   r.edge_cost8 = edge_cost8();
   r.dbg = g_dbg;
   // dynamic tail: a counter slot from the per-device pool (self-resetting)
-  r.tail_counter = split_param(0) < 1024 ? tail_counter_slot() : nullptr;
+  r.tail_counter = split_param(0) < 1024 ? tail_counter_slot(r.stream) : nullptr;
   r.static_frac = split_param(0);
   r.tail_rows = split_param(1);
   r.strip_align = split_param(2);
@@ -534,7 +578,7 @@ int run_fused(const b2dwt_plan_s& p, FusedLaunch& r) {
         if (q.out_pl[c]) q.out_pl[c] = static_cast<char*>(q.out_pl[c]) + ob;
       }
       q.batch = i1 - i0;
-      if (i > 0) q.tail_counter = r.tail_counter ? tail_counter_slot() : nullptr;
+      if (i > 0) q.tail_counter = r.tail_counter ? tail_counter_slot(r.stream) : nullptr;
       e = b.launch(q, &used_tma);
     }
   } else {
@@ -543,12 +587,86 @@ int run_fused(const b2dwt_plan_s& p, FusedLaunch& r) {
       FusedLaunch q = r;
       q.row_begin = rb + static_cast<int>((re - rb) * i / parts);
       q.row_end = rb + static_cast<int>((re - rb) * (i + 1) / parts);
-      if (i > 0) q.tail_counter = r.tail_counter ? tail_counter_slot() : nullptr;
+      if (i > 0) q.tail_counter = r.tail_counter ? tail_counter_slot(r.stream) : nullptr;
       e = b.launch(q, &used_tma);
     }
   }
   if (e == cudaErrorNotSupported) return fail(B2DWT_EUNSUPPORTED, "no compiled fused variant for this request");
   if (e != cudaSuccess) return cuda_fail(e, "fused stream kernel");
+  return B2DWT_OK;
+}
+
+// Smallest level (quads) the two-level fused kernel takes; below it the levels
+// run one launch each.  B2DWT_FUSE2_MIN_QUADS overrides (0 disables fusion).
+int64_t fuse2_min_quads() {
+  const char* e = std::getenv("B2DWT_FUSE2_MIN_QUADS");  // read per call: tests vary it
+  return e ? std::atoll(e) : int64_t{1} << 20;
+}
+
+// Levels l and l+1 of a forward pyramid in one kernel (fused2_kernel.cuh):
+// level l's LL never reaches HBM.  B2DWT_EUNSUPPORTED when the request does not
+// fit it (the caller then runs the two levels separately).
+int run_fused2_pair(const b2dwt_plan_s& p, const void* in, int64_t in_ld, int64_t h, int64_t w,
+                    const b2dwt_planes& det0, const b2dwt_planes& det1, void* ll1, int64_t ll1_ld,
+                    cudaStream_t stream, bool any_size = false) {
+  if (p.builtin < 0 || (p.flags & (B2DWT_FORCE_GENERIC | B2DWT_NO_TMA | B2DWT_NO_FUSE)) || p.dtype != B2DWT_F32)
+    return B2DWT_EUNSUPPORTED;
+  const Builtin& b = builtins()[p.builtin];
+  if (b.inverse) return B2DWT_EUNSUPPORTED;
+  const int64_t rows = h / 2, cols = w / 2;
+  const int64_t minq = fuse2_min_quads();
+  if (!any_size && (minq <= 0 || rows * cols < minq)) return B2DWT_EUNSUPPORTED;
+  if ((rows & 1) || (cols & 1)) return B2DWT_EUNSUPPORTED;
+  Fused2Launch r{};
+  r.dtype = 0;
+  r.strict = strict_of(&p);
+  r.in_img = in;
+  r.in_ld = in_ld;
+  r.rows = static_cast<int>(rows);
+  r.cols = static_cast<int>(cols);
+  for (int c = 1; c < 4; ++c) {
+    r.out0_pl[c] = det0.ptr[c];
+    r.out0_ld[c] = det0.ld[c];
+    r.out1_pl[c] = det1.ptr[c];
+    r.out1_ld[c] = det1.ld[c];
+  }
+  r.out1_pl[0] = ll1;
+  r.out1_ld[0] = ll1_ld;
+  // work split of the fused kernel: a unit re-reads the cones of BOTH levels
+  // (~14 level-l rows), so its dynamic tail chunks are longer than the stream
+  // kernel's.  B2DWT_F2_STATIC_FRAC / B2DWT_F2_TAIL_ROWS override.
+  static const int f2_static = [] {
+    const char* e = std::getenv("B2DWT_F2_STATIC_FRAC");
+    return e ? std::atoi(e) : 832;
+  }();
+  static const int f2_tail = [] {
+    const char* e = std::getenv("B2DWT_F2_TAIL_ROWS");
+    return e ? std::atoi(e) : 48;
+  }();
+  r.static_frac = f2_static;
+  r.tail_rows1 = f2_tail;
+  r.min_rows1 = std::max(8, min_rows() / 2);
+  r.pdl = split_param(4) != 0;
+  r.stream = stream;
+  // footprint-bounded launches, as run_fused: row bands of <= max_launch_bytes of input
+  const int64_t rows1 = rows / 2;
+  const int64_t in_bytes = rows * cols * 16;
+  const int64_t cap = max_launch_bytes();
+  int64_t parts = cap > 0 ? (in_bytes + cap - 1) / cap : 1;
+  parts = std::max<int64_t>(1, std::min<int64_t>(parts, rows1 / 128));
+  cudaError_t e = cudaSuccess;
+  for (int64_t i = 0; i < parts && e == cudaSuccess; ++i) {
+    r.k_begin = static_cast<int>(rows1 * i / parts);
+    r.k_end = static_cast<int>(rows1 * (i + 1) / parts);
+    r.tail_counter = f2_static < 1024 ? tail_counter_slot(stream) : nullptr;
+    e = b.fused2(r);
+    if (e == cudaErrorNotSupported) {
+      (void)cudaGetLastError();
+      if (i == 0) return B2DWT_EUNSUPPORTED;
+      return fail(B2DWT_ECUDA, "two-level fused kernel refused a later row band");
+    }
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "two-level fused kernel");
   return B2DWT_OK;
 }
 
@@ -922,6 +1040,23 @@ int b2dwt_dwt(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t heig
   int64_t in_ld = image_ld;
   for (int l = 0; l < levels; ++l) {
     const int64_t h = height >> l, w = width >> l;
+    if (l + 1 < levels) {
+      // levels l and l+1 in one kernel when the plan and geometry allow it
+      void* ll1 = l + 1 == levels - 1 ? ll_out : sc[(l + 1) & 1];
+      const int64_t ll1_ld = l + 1 == levels - 1 ? ll_ld : w / 4;
+      char name[40];
+      std::snprintf(name, sizeof(name), "b2dwt dwt levels %d+%d", l, l + 1);
+      NvtxRange range(name);
+      const int rc = run_fused2_pair(*plan, in, in_ld, h, w, details[l], details[l + 1], ll1, ll1_ld,
+                                     static_cast<cudaStream_t>(stream));
+      if (rc == B2DWT_OK) {
+        in = ll1;
+        in_ld = ll1_ld;
+        ++l;
+        continue;
+      }
+      if (rc != B2DWT_EUNSUPPORTED) return rc;
+    }
     const b2dwt_planes& o = details[l];
     b2dwt_planes lv = o;
     lv.bstride = 0;
@@ -940,6 +1075,24 @@ int b2dwt_dwt(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t heig
     in_ld = lv.ld[0];
   }
   return B2DWT_OK;
+}
+
+int b2dwt_forward2(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t height, int64_t width,
+                   const b2dwt_planes* det0, const b2dwt_planes* out1, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (!image || !det0 || !out1) return fail(B2DWT_EINVAL, "null pointer");
+  if (height % 4 || width % 4 || height < 4 || width < 4)
+    return fail(B2DWT_EINVAL, "height and width must be divisible by 4");
+  if (int rc = check_dims(height, width)) return rc;
+  if (image_ld < width) return fail(B2DWT_EINVAL, "image_ld < width");
+  for (int c = 1; c < 4; ++c)
+    if (!det0->ptr[c] || det0->ld[c] < width / 2) return fail(B2DWT_EINVAL, "bad level-0 detail plane");
+  for (int c = 0; c < 4; ++c)
+    if (!out1->ptr[c] || out1->ld[c] < width / 4) return fail(B2DWT_EINVAL, "bad level-1 plane");
+  const int rc = run_fused2_pair(*plan, image, image_ld, height, width, *det0, *out1, out1->ptr[0], out1->ld[0],
+                                 static_cast<cudaStream_t>(stream), /*any_size=*/true);
+  if (rc == B2DWT_EUNSUPPORTED) return fail(rc, "request does not fit the two-level fused kernel");
+  return rc;
 }
 
 int b2dwt_idwt(b2dwt_plan plan, const void* ll, int64_t ll_ld, const b2dwt_planes* details, int32_t levels,

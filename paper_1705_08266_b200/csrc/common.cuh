@@ -46,7 +46,10 @@ __device__ __forceinline__ int reflect(int i, int parity, int cs) {
 
 // Arithmetic policies.  Strict: separately rounded IEEE multiply and add in
 // the compiled order -- NumPy's `acc = x*k; acc += x*k` (engine.py:350-362).
-// Fast: fused multiply-add in the same order.
+// Fast: fused multiply-add in the same order -- and ONLY there: the leading
+// product and unit additions stay separately rounded, so the compiler cannot
+// contract them differently in different kernels (stream, tile, two-level
+// fused) and every fast kernel computes the same bits.
 template <bool kStrict>
 struct Arith;
 template <>
@@ -62,12 +65,24 @@ struct Arith<true> {
 };
 template <>
 struct Arith<false> {
-  static __device__ __forceinline__ float mul(float x, float k) { return x * k; }
-  static __device__ __forceinline__ double mul(double x, double k) { return x * k; }
-  static __device__ __forceinline__ float add(float a, float b) { return a + b; }
-  static __device__ __forceinline__ double add(double a, double b) { return a + b; }
+  static __device__ __forceinline__ float mul(float x, float k) { return __fmul_rn(x, k); }
+  static __device__ __forceinline__ double mul(double x, double k) { return __dmul_rn(x, k); }
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
   static __device__ __forceinline__ float mac(float acc, float x, float k) { return fmaf(x, k, acc); }
   static __device__ __forceinline__ double mac(double acc, double x, double k) { return fma(x, k, acc); }
+};
+
+// Fast mode's one contraction, made explicit: when a target's first term is a
+// product and its second a unit term, the pair is evaluated as one fused
+// multiply-add, fma(x0, k0, x1) (what a contracting compiler would emit for
+// x0 * k0 + x1, but fixed here so every kernel computes the same bits).
+// defer(K, count, unit_K, unit_next): term K's product is deferred to K + 1.
+template <bool kStrict>
+struct FastJoin {
+  B2DWT_HD static constexpr bool defer(int k, int count, bool unit_k, bool unit_next) {
+    return !kStrict && k == 0 && count > 1 && !unit_k && unit_next;
+  }
 };
 
 }  // namespace b2dwt

@@ -1,0 +1,490 @@
+// fused2_kernel.cuh -- TWO pyramid levels in one kernel (sm_100a).
+//
+// The multi-level forward transform (level l+1 is
+// `forward` of level l's LL, liftfuse/engine.py:481-487 iterated) normally
+// writes level l's LL band to HBM and reads it back for level l+1.  Here the
+// LL band never leaves the SM: each CTA runs level l's register pipeline
+// (stream_kernel.cuh, Q = 2 quads per lane) over a super-strip of columns,
+// passes the LL rows between its four warps through a small shared-memory
+// ring, and the same warps run level l+1's pipeline (Q = 1) on them.  HBM
+// traffic per pair of levels drops from 1 read + 1 write of each level's input
+// to 1 read of level l's input + 1 write of level l's HL/LH/HH and of level
+// l+1's four planes -- the paper's "keep intermediate results on chip across
+// overlapping blocks" applied across levels.
+//
+// Geometry (all built-in lifting programs: per-sub-step horizontal reach <= 1,
+// cone <= 2 quads per side):
+//   CTA super-strip c owns level-l quad columns [208c, 208c + 208) and level
+//   l+1 columns [104c, 104c + 104) (both whole 32-B sectors in f32).
+//   Level l:   warp w loads quads m0 + [0, 64), m0 = 208c - 8 + 56w (32-B
+//              aligned), keeps the LL of lanes 2..29 (quads m0 + [4, 60), inside
+//              its valid cone) and stores HL/LH/HH of its share of the CTA's
+//              columns (56-quad warp boundaries: whole sectors).
+//   Ring:      level-(l+1) quads: slot[j] = (c0, c1, c2, c3) of level-(l+1)
+//              column 104c - 2 + j, j in [0, 112); level-l lane l of warp w
+//              writes j = 28w + l - 2 (even LL row: c0/c1, odd row: c2/c3).
+//   Level l+1: warp w, lane l runs column 104c - 2 + 26w + l (Q = 1) and stores
+//              [104c + 26w, +26) (valid lanes are 2..29).
+// Warp w reads ring columns of warps w-1 and w+1 and they read its columns, so
+// each warp signals one mbarrier per ring slot (32 arrivals) and waits only for
+// its neighbours' -- which also proves they are done reading the slot it is
+// about to reuse (kF2Ring >= 2 steps later).  The ring depth is the slack
+// between the warps of a CTA.
+//
+// Rows: a work unit is (super-strip, level-(l+1) rows [k0, k1)).  Level l then
+// computes valid LL rows [2(k0 - up1), 2(k1 + down1)) (cone of level l+1) and
+// stores HL/LH/HH rows [2 k0, 2 k1); vertically interior units run both
+// pipelines entirely unchecked (the stream kernel's fill argument: extra ticks
+// compute rows outside every stored row's cone).  Boundary semantics, term
+// order and arithmetic are exactly the stream kernel's, so results are
+// bit-identical to two separate launches (tests/test_gpu_fused2.py).
+#pragma once
+
+#include "stream_kernel.cuh"
+
+namespace b2dwt {
+
+constexpr int kF2SuperW = 208;  // level-l quads per CTA super-strip
+constexpr int kF2StripW = 56;   // level-l quads between the warps' strips
+constexpr int kF2Lead = 8;      // level-l quads loaded left of the CTA's columns
+#ifndef B2DWT_F2_RING
+#define B2DWT_F2_RING 6
+#endif
+constexpr int kF2Ring = B2DWT_F2_RING;  // ring slots (level-(l+1) rows)
+constexpr int kF2J = 112;               // ring columns (level-(l+1) quads)
+constexpr int kF2W1 = 26;               // level-(l+1) columns stored per warp
+constexpr int kF2Edge = 8;      // level-(l+1) rows at the image top / bottom run as checked units
+
+template <class T>
+struct Fused2Args {
+  // level-l image (interleaved), buffer row 0 == global quad row 0
+  const T* in_img;
+  const T* in_pl[4];  // unused (RowSource interface)
+  int64_t in_ld[4];
+  int64_t in_bstride;
+  int in_row0;
+  int in_row_end;
+  // level-l HL/LH/HH ([0] unused: the LL band stays on chip)
+  T* out_pl[4];
+  int64_t out_ld[4];
+  int out_row0;
+  // level-(l+1) LL/HL/LH/HH
+  T* out1_pl[4];
+  int64_t out1_ld[4];
+  int rows, cols;      // level-l quad grid
+  int k_begin, k_end;  // level-(l+1) quad rows produced by this launch
+  int n_super;         // CTA super-strips
+  int n_ctas;
+  unsigned long long* tail_counter;  // [0] tickets, [1] CTAs done (self-resetting), or null
+  int tail_chunk;                    // level-(l+1) rows per dynamic chunk
+  // work space (f2_work_space on the host): interior rows [ki0, ki0 + rows_in)
+  // of every super-strip, unit cost = one level-(l+1) row; [0, static_end)
+  // split evenly over the CTAs; dynamic items = the `top` / `bot` edge units of
+  // every super-strip (n_edge), then tail chunks of [static_end, total)
+  int top, bot, ki0, rows_in, n_edge;
+  int total, static_end, n_dyn;
+};
+
+// Host: fill the work-space fields of `a` (its k range, n_super, tail_counter,
+// tail_chunk and rows already set).  The rows within kF2Edge of the image top /
+// bottom need the checked (reflecting) path at both levels and run as short
+// separate units, so no long segment is ever checked.
+template <class T>
+inline void f2_work_space(Fused2Args<T>& a, int static_frac) {
+  const int rows1 = a.rows / 2;
+  a.top = a.k_begin == 0 ? (a.k_end - a.k_begin < kF2Edge ? a.k_end - a.k_begin : kF2Edge) : 0;
+  const int rest = a.k_end - a.k_begin - a.top;
+  a.bot = a.k_end == rows1 ? (rest < kF2Edge ? rest : kF2Edge) : 0;
+  a.ki0 = a.k_begin + a.top;
+  a.rows_in = a.k_end - a.bot - a.ki0;
+  a.n_edge = (a.top > 0 ? a.n_super : 0) + (a.bot > 0 ? a.n_super : 0);
+  a.total = a.n_super * a.rows_in;
+  a.static_end = a.tail_counter != nullptr ? static_cast<int>(static_cast<int64_t>(a.total) * static_frac / 1024)
+                                           : a.total;
+  a.n_dyn = a.n_edge + (a.total - a.static_end + a.tail_chunk - 1) / a.tail_chunk;
+}
+
+// Level-l sink: HL/LH/HH straight to HBM (8-B vectors), LL into the ring.
+template <class T>
+struct F2Sink0 {
+  char* base[4];
+  int ldb[4];
+  bool full, vec, any_scalar;
+  unsigned mask;
+  unsigned ring;  // shared address of this lane's ring column in slot 0, or 0 (lane does not publish)
+  int slot;       // current ring slot
+  int last_n;
+
+  __device__ __forceinline__ void init(const Fused2Args<T>& a, int m_lane, int vlo, int vhi) {
+    bool v = true;
+    mask = 0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (m_lane + q >= vlo && m_lane + q < vhi) mask |= 1u << q;
+    full = mask == 3u;
+#pragma unroll
+    for (int c = 1; c < 4; ++c) {
+      ldb[c] = static_cast<int>(a.out_ld[c] * static_cast<int64_t>(sizeof(T)));
+      T* p = a.out_pl[c] - static_cast<int64_t>(a.out_row0) * a.out_ld[c] + m_lane;
+      base[c] = reinterpret_cast<char*>(p);
+      v = v && (a.out_ld[c] % 2 == 0) && (reinterpret_cast<uintptr_t>(p) % (sizeof(T) * 2) == 0);
+    }
+    vec = v;
+    any_scalar = __any_sync(0xffffffffu, mask != 0 && !(full && vec));
+    last_n = -0x40000000;
+  }
+
+  template <bool kScalar>
+  __device__ __forceinline__ void store(const T (&v)[4][2], int n, bool in_range) {
+    const bool vok = in_range && full && vec;
+#pragma unroll
+    for (int c = 1; c < 4; ++c) {
+      char* p = base[c] + static_cast<int64_t>(n) * ldb[c];
+      st_pred<T, 2>(p, v[c], vok);
+      if (kScalar && any_scalar) {
+        if (in_range && !(full && vec)) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            if (mask & (1u << q)) reinterpret_cast<T*>(p)[q] = v[c][q];
+        }
+      }
+    }
+    // LL row n: level-(l+1) components (n even: c0, c1; odd: c2, c3)
+    if (ring != 0) {
+      const unsigned r = ring + static_cast<unsigned>(slot * (kF2J * 4) + 2 * (n & 1)) * sizeof(T);
+      if constexpr (sizeof(T) == 4) {
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};\n" ::"r"(r), "f"(v[0][0]), "f"(v[0][1]) : "memory");
+      } else {
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(r), "d"(v[0][0]), "d"(v[0][1]) : "memory");
+      }
+    }
+    last_n = n;
+  }
+};
+
+// Level-(l+1) sink: one value per plane and lane.  Addresses are formed from
+// the kernel parameters (constant bank) at each store instead of being held in
+// registers: the level-l pipeline needs those registers.
+template <class T>
+struct F2Sink1 {
+  const Fused2Args<T>* a;  // the __grid_constant__ parameter block
+  int m_lane;
+  bool lane_ok;
+  bool any_scalar;  // (StoreSink interface; never set)
+
+  template <bool kScalar>
+  __device__ __forceinline__ void store(const T (&v)[4][1], int n, bool in_range) {
+    if (in_range && lane_ok) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) a->out1_pl[c][static_cast<int64_t>(n) * a->out1_ld[c] + m_lane] = v[c][0];
+    }
+  }
+};
+
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_sa(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// Per-warp state of the level-(l+1) half.
+template <class P, class T, bool kStrict>
+struct F2Level1 {
+  using Pipe = Stage<P, T, 1, kStrict, 0>;
+  Pipe pipe;
+  F2Sink1<T> sink;
+  Ctx cx;
+  unsigned rd;    // shared address of this lane's ring column (slot 0)
+  unsigned bars;  // shared address of the ring mbarriers [slot][warp]
+  int warp;
+  unsigned u;     // level-(l+1) steps taken by this CTA (ring slot / phase)
+  int last_load;  // last level-(l+1) input row that exists
+
+  // Publish this warp's LL pair for step u, wait for the neighbour warps',
+  // read this lane's level-(l+1) input row.
+  __device__ __forceinline__ void gather(T (&row)[4][1]) {
+    const unsigned s = u % kF2Ring, par = (u / kF2Ring) & 1u;
+    const unsigned b = bars + (s * 4) * 8;
+    mbar_arrive(b + warp * 8);
+#ifndef B2DWT_F2_NOSYNC  // (timing experiment only: results are wrong without it)
+    if (warp > 0) mbar_wait_sa(b + (warp - 1) * 8, par);
+    if (warp < 3) mbar_wait_sa(b + (warp + 1) * 8, par);
+#endif
+    __syncwarp();  // the warp's own lanes' ring writes
+    const unsigned p = rd + s * (kF2J * 4) * static_cast<unsigned>(sizeof(T));
+    if constexpr (sizeof(T) == 4) {
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                   : "=f"(row[0][0]), "=f"(row[1][0]), "=f"(row[2][0]), "=f"(row[3][0])
+                   : "r"(p)
+                   : "memory");
+    } else {
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(row[0][0]), "=d"(row[1][0]) : "r"(p) : "memory");
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(row[2][0]), "=d"(row[3][0]) : "r"(p + 16) : "memory");
+    }
+    ++u;
+  }
+
+  // Unchecked level-(l+1) tick at compile-time phase PH1.
+  template <int PH1, int HEDGE, class Args>
+  __device__ __forceinline__ void step(int t1, const Args& a) {
+    T row[4][1];
+    gather(row);
+    pipe.template tick<PH1, false, HEDGE>(row, t1, cx, a, sink);
+  }
+
+  // Checked level-(l+1) tick (runtime phase, row-range tests, edge remaps).
+  template <class Args>
+  __device__ __forceinline__ void step_checked(int t1, const Args& a) {
+    T row[4][1];
+    gather(row);
+    checked_tick<Geo<P>::kPeriod>(pipe, row, t1, cx, a, sink, std::make_integer_sequence<int, Geo<P>::kPeriod>{});
+  }
+
+  // Level-(l+1) rows past the image bottom: no input (zeros, never read).
+  template <class Args>
+  __device__ __forceinline__ void flush_checked(int t1, const Args& a) {
+    const T row[4][1] = {{T(0)}, {T(0)}, {T(0)}, {T(0)}};
+    checked_tick<Geo<P>::kPeriod>(pipe, row, t1, cx, a, sink, std::make_integer_sequence<int, Geo<P>::kPeriod>{});
+  }
+};
+
+// 2kP unchecked level-l ticks t .. t+2kP-1 (t % 2kP == 0); after every tick
+// that completes an LL row pair, one level-(l+1) tick (L1C: checked).
+template <int HEDGE, class P, class T, bool kStrict, class Pipe0, class Src, class Sink0, class Args, int... I>
+__device__ __forceinline__ void f2_steady_chunk(Pipe0& pipe0, Src& src, F2Level1<P, T, kStrict>& l1, int t,
+                                                const Ctx& cx0, const Args& a, Sink0& sink0,
+                                                const CUtensorMap* m, std::integer_sequence<int, I...>) {
+  constexpr int kD0 = Geo<P>::down;
+  constexpr int kP = Geo<P>::kPeriod;
+  constexpr bool kNest = Src::kStageRows % static_cast<int>(sizeof...(I)) == 0;
+  auto one = [&](auto ic) {
+    constexpr int i = decltype(ic)::value;
+    T row[4][2];
+    if constexpr (kNest)
+      src.next_row(row);
+    else
+      src.next(row, a, m, m, m, m);
+    pipe0.template tick<i, false, HEDGE>(row, t + i, cx0, a, sink0);
+    if constexpr (((i - kD0) % 2 + 2) % 2 == 1) {  // LL row t + i - kD0 is odd: a quad row is complete
+      sink0.slot = static_cast<int>((l1.u + 1) % kF2Ring);
+      l1.template step<cmod((i - kD0 - 1) / 2, kP), HEDGE>((t + i - kD0 - 1) / 2, a);
+    }
+  };
+  if constexpr (kNest) src.advance_if_due(a, m, m, m, m);  // t % period == 0: the only possible stage switch
+  (one(std::integral_constant<int, I>{}), ...);
+}
+
+#ifndef B2DWT_F2_MIN_CTAS
+#define B2DWT_F2_MIN_CTAS 3
+#endif
+template <class P, class T, bool kStrict, int STAGES, int RPS>
+__global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
+    fused2_kernel(const __grid_constant__ Fused2Args<T> a, const __grid_constant__ CUtensorMap tmap) {
+  constexpr int WARPS = 4, Q0 = 2;
+  using G = Geo<P>;
+  using Src = RowSource<T, Q0, kLayoutInterleaved, true, STAGES, RPS>;
+  using Pipe0 = Stage<P, T, Q0, kStrict, 0>;
+  constexpr int kP = G::kPeriod;
+  constexpr int kPF = 2 * kP * B2DWT_UNROLL;  // one fused chunk: 2kP level-l ticks = kP level-(l+1) ticks (x unroll)
+  static_assert(G::left <= 2 && G::right <= 2, "fused levels need a cone of <= 2 quads per side");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+
+  const int warp = threadIdx.x / kLaneCount;
+  const int lane = threadIdx.x % kLaneCount;
+  const int cta = blockIdx.x;
+  if (cta >= a.n_ctas) return;
+  __shared__ unsigned long long s_ticket;
+
+  // shared memory: per-warp TMA rings | their mbarriers | LL ring | its mbarriers [slot][warp]
+  const size_t ring0_bytes = static_cast<size_t>(WARPS) * STAGES * Src::kStageElems * sizeof(T);
+  const unsigned ll_ring = static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) +
+                           static_cast<unsigned>(ring0_bytes + WARPS * STAGES * sizeof(uint64_t));
+  const unsigned ll_bars = ll_ring + kF2Ring * kF2J * 4 * static_cast<unsigned>(sizeof(T));
+
+  Src src;
+  src.ring = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(warp) * STAGES * Src::kStageElems;
+  src.bars = reinterpret_cast<uint64_t*>(smem_raw + ring0_bytes) + warp * STAGES;
+  src.lane = lane;
+  src.cols = a.cols;
+  src.init_barriers(&tmap, &tmap, &tmap, &tmap);
+  for (int i = threadIdx.x; i < kF2Ring * kF2J * 4; i += WARPS * kLaneCount) {
+    const unsigned p = ll_ring + static_cast<unsigned>(i * sizeof(T));
+    if constexpr (sizeof(T) == 4)
+      asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(p), "f"(0.0f) : "memory");
+    else
+      asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(p), "d"(0.0) : "memory");
+  }
+  if (threadIdx.x < kF2Ring * WARPS) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(ll_bars + threadIdx.x * 8), "r"(kLaneCount));
+  }
+  fence_mbar_init();
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  const int rows1 = a.rows / 2, cols1 = a.cols / 2;
+  // work space: see Fused2Args / f2_work_space
+  int f = static_cast<int>(static_cast<int64_t>(a.static_end) * cta / a.n_ctas);
+  int f_end = static_cast<int>(static_cast<int64_t>(a.static_end) * (cta + 1) / a.n_ctas);
+  int item = cta;  // next dynamic item without a counter: round robin
+
+  F2Level1<P, T, kStrict> l1;
+  l1.bars = ll_bars;
+  l1.warp = warp;
+  l1.u = 0;
+  l1.rd = ll_ring + static_cast<unsigned>((kF2W1 * warp + lane) * 4 * sizeof(T));
+  const unsigned ring_w =  // this lane's published column (lanes 2..29), or 0
+      lane >= 2 && lane < 30 ? ll_ring + static_cast<unsigned>((28 * warp + lane - 2) * 4 * sizeof(T)) : 0u;
+
+#pragma unroll 1
+  for (;;) {
+    // next unit: super-strip `sup`, level-(l+1) rows [k0, k1) (CTA-uniform)
+    int sup, k0, k1;
+    if (f < f_end) {  // static share: [f, f_end) of the interior cost space
+      sup = f / a.rows_in;
+      const int c0 = sup * a.rows_in;
+      k0 = a.ki0 + (f - c0);
+      k1 = a.ki0 + min(a.rows_in, f_end - c0);
+      f = c0 + a.rows_in;
+      if (k0 >= k1) continue;
+    } else {  // next dynamic item
+      int j;
+      if (a.tail_counter != nullptr) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_ticket = atomicAdd(a.tail_counter, 1ull);
+        __syncthreads();
+        j = static_cast<int>(min(s_ticket, static_cast<unsigned long long>(a.n_dyn)));
+      } else {
+        j = item;
+        item += a.n_ctas;
+      }
+      if (j >= a.n_dyn) break;
+      if (j >= a.n_edge) {
+        f = a.static_end + (j - a.n_edge) * a.tail_chunk;
+        f_end = min(a.total, f + a.tail_chunk);
+        continue;
+      }
+      const bool is_top = a.top > 0 && j < a.n_super;
+      sup = is_top ? j : j - (a.top > 0 ? a.n_super : 0);
+      k0 = is_top ? a.k_begin : a.k_end - a.bot;
+      k1 = is_top ? a.k_begin + a.top : a.k_end;
+    }
+    // level l: valid LL rows [n0p, n1p), HL/LH/HH rows [2 k0, 2 k1) stored
+    const int n0p = max(0, 2 * (k0 - G::up));
+    const int n1p = min(a.rows, 2 * (k1 + G::down));
+    Ctx cx;
+    cx.rows = a.rows;
+    cx.cols = a.cols;
+    cx.fold1 = true;  // host guarantees cols >= 128
+    cx.m_strip = kF2SuperW * sup - kF2Lead + kF2StripW * warp;
+    cx.m_lane = cx.m_strip + Q0 * lane;
+    const bool hedge0 = cx.m_strip < 0 || cx.m_strip + Q0 * kLaneCount > a.cols;
+    cx.hedge = hedge0;
+    cx.n0 = 2 * k0;
+    cx.n1 = 2 * k1;
+    cx.first = max(0, n0p - G::up);
+    const int last_load = min(a.rows - 1, n1p - 1 + G::down);
+    const int last_tick = n1p - 1 + G::down;
+
+    // level l+1
+    l1.cx.rows = rows1;
+    l1.cx.cols = cols1;
+    l1.cx.fold1 = true;  // cols1 >= 64
+    l1.cx.m_strip = kF2SuperW / 2 * sup - 2 + kF2W1 * warp;
+    l1.cx.m_lane = l1.cx.m_strip + lane;
+    const bool hedge1 = l1.cx.m_strip < 0 || l1.cx.m_strip + kLaneCount > cols1;
+    l1.cx.hedge = hedge1;
+    l1.cx.n0 = k0;
+    l1.cx.n1 = k1;
+    l1.cx.first = max(0, k0 - G::up);
+    l1.last_load = min(rows1 - 1, k1 + G::down - 1);
+    const int last_tick1 = k1 - 1 + G::down;
+
+    const int t_lo = (cx.first / kPF) * kPF;
+    const int t_hi = ((last_tick + kPF) / kPF) * kPF;
+    const bool unchecked = 2 * (k0 - G::up) - G::up >= 0 && last_tick < a.rows && t_hi <= a.rows &&
+                           k0 - G::up >= 0 && last_tick1 < rows1;
+    src.first = unchecked ? t_lo : cx.first;
+    src.last_load = unchecked ? t_hi - 1 : last_load;
+    src.m_lane = cx.m_lane;
+    src.m_strip = cx.m_strip;
+    src.b = 0;
+    src.boff = 0;
+    src.start(a, &tmap, &tmap, &tmap, &tmap);
+
+    F2Sink0<T> sink0;
+    {
+      const int own0 = kF2SuperW * sup, own1 = min(a.cols, own0 + kF2SuperW);
+      const int w0 = cx.m_strip + 4, w1 = cx.m_strip + 60;  // this warp's published LL columns
+      sink0.init(a, cx.m_lane, max(own0, w0), min(own1, w1));
+      sink0.ring = ring_w;
+      sink0.slot = static_cast<int>(l1.u % kF2Ring);
+    }
+    {
+      const int own0 = kF2SuperW / 2 * sup + kF2W1 * warp;
+      l1.sink.a = &a;
+      l1.sink.m_lane = l1.cx.m_lane;
+      l1.sink.lane_ok = l1.cx.m_lane >= own0 && l1.cx.m_lane < min(cols1, own0 + kF2W1);
+      l1.sink.any_scalar = false;
+    }
+    Pipe0 pipe0{};
+    l1.pipe = typename F2Level1<P, T, kStrict>::Pipe{};
+    const bool hedge_any = hedge0 || hedge1 || sink0.any_scalar || l1.sink.any_scalar;
+
+    if (unchecked) {
+      // both levels interior: whole fused periods, no tests
+      if (hedge_any) {
+#pragma unroll 1
+        for (int t = t_lo; t < t_hi; t += kPF)
+          f2_steady_chunk<1>(pipe0, src, l1, t, cx, a, sink0, &tmap, std::make_integer_sequence<int, kPF>{});
+      } else {
+#pragma unroll 1
+        for (int t = t_lo; t < t_hi; t += kPF)
+          f2_steady_chunk<0>(pipe0, src, l1, t, cx, a, sink0, &tmap, std::make_integer_sequence<int, kPF>{});
+      }
+    } else {
+      // image top / bottom (short units): every tick checked at both levels
+#pragma unroll 1
+      for (int t = cx.first; t <= last_tick; ++t) {
+        T row[4][2];
+        if (t <= last_load) {
+          src.next(row, a, &tmap, &tmap, &tmap, &tmap);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) row[c][q] = T(0);
+        }
+        checked_tick<kP>(pipe0, row, t, cx, a, sink0, std::make_integer_sequence<int, kP>{});
+        if ((sink0.last_n & 1) && sink0.last_n >= 0) {  // an LL row pair is complete
+          const int t1 = (sink0.last_n - 1) / 2;
+          sink0.last_n = -0x40000000;
+          sink0.slot = static_cast<int>((l1.u + 1) % kF2Ring);
+          l1.step_checked(t1, a);
+        }
+      }
+      // level-(l+1) rows whose cone runs past the image bottom: flush ticks
+#pragma unroll 1
+      for (int t1 = l1.last_load + 1; t1 <= last_tick1; ++t1) l1.flush_checked(t1, a);
+    }
+    src.finish();
+  }
+  if (a.tail_counter != nullptr && threadIdx.x == 0) {
+    if (atomicAdd(a.tail_counter + 1, 1ull) == static_cast<unsigned long long>(a.n_ctas) - 1) {
+      a.tail_counter[0] = 0;
+      a.tail_counter[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+}  // namespace b2dwt

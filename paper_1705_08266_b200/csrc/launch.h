@@ -43,6 +43,29 @@ struct FusedLaunch {
   cudaStream_t stream;
 };
 
+// Two pyramid levels in one launch (fused2_kernel.cuh): level l of an
+// interleaved f32 image (rows x cols quads) and level l+1 of its LL band, which
+// never leaves the SM.  Level l's HL/LH/HH go to out0_pl[1..3]; level l+1's
+// LL/HL/LH/HH to out1_pl[0..3]; level-(l+1) quad rows [k_begin, k_end).
+struct Fused2Launch {
+  int dtype;  // 0 f32 (only)
+  bool strict;
+  const void* in_img;
+  int64_t in_ld;
+  int rows, cols;
+  void* out0_pl[4];
+  int64_t out0_ld[4];
+  void* out1_pl[4];
+  int64_t out1_ld[4];
+  int k_begin, k_end;
+  unsigned long long* tail_counter;
+  int static_frac;
+  int tail_rows1;
+  int min_rows1;
+  bool pdl;
+  cudaStream_t stream;
+};
+
 // RAII NVTX range (b2dwt_host.cu); a no-op unless B2DWT_NVTX is set.
 struct NvtxRange {
   explicit NvtxRange(const char* name);
@@ -61,5 +84,6 @@ struct ConeInfo {
 using FusedLauncher = cudaError_t (*)(const FusedLaunch&, bool* used_tma);
 using TileLauncher = cudaError_t (*)(const FusedLaunch&);
 using ConeGetter = ConeInfo (*)();
+using Fused2Launcher = cudaError_t (*)(const Fused2Launch&);
 
 }  // namespace b2dwt

@@ -315,15 +315,24 @@ struct Stage<P, T, Q, kStrict, S, false> {
 
   template <int OFF, int TGT, int K, class Args>
   __device__ __forceinline__ static void term(const T (&win)[NW][4][E], T (&acc)[Q], const Args& a) {
-    constexpr int idx = P::begin(S * 4 + TGT) + K;
+    constexpr int base = P::begin(S * 4 + TGT);
+    constexpr int idx = base + K;
+    constexpr int cnt = P::begin(S * 4 + TGT + 1) - base;
     constexpr TermInfo ti = P::term(idx);
     constexpr int slot = cmod(OFF + ti.dn, NW);
+    // fast mode: a leading product followed by a unit term is ONE fused
+    // multiply-add (FastJoin, common.cuh)
+    constexpr bool kDefer = FastJoin<kStrict>::defer(K, cnt, ti.unit, K + 1 < cnt && P::term(idx + 1).unit);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const T x = win[slot][ti.src][L + q + ti.dm];
       constexpr T kc = static_cast<T>(P::coef(idx));  // liftfuse: dtype.type(coeff), engine.py:357
       if constexpr (K == 0) {
-        acc[q] = ti.unit ? x : Ar::mul(x, kc);
+        if constexpr (!kDefer) acc[q] = ti.unit ? x : Ar::mul(x, kc);
+      } else if constexpr (K == 1 && FastJoin<kStrict>::defer(0, cnt, P::term(base).unit, ti.unit)) {
+        constexpr TermInfo t0 = P::term(base);
+        constexpr T k0 = static_cast<T>(P::coef(base));
+        acc[q] = Ar::mac(x, win[cmod(OFF + t0.dn, NW)][t0.src][L + q + t0.dm], k0);
       } else {
         acc[q] = ti.unit ? Ar::add(acc[q], x) : Ar::mac(acc[q], x, kc);
       }
@@ -588,6 +597,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+// The same wait with a value the caller needs right after it as an asm input,
+// so it is materialised (e.g. reloaded from a spill slot) BEFORE the wait.
+__device__ __forceinline__ void mbar_wait_keep(uint64_t* bar, unsigned parity, int keep) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(b),
+      "r"(parity), "r"(keep)
+      : "memory");
+}
 __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -602,6 +625,19 @@ __device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* map, 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(b), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
+
+// L2 prefetch of a TMA box (no shared memory, no completion): warms L2 for a
+// ring stage that will be loaded later.
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+
+#ifndef B2DWT_L2_PREFETCH
+#define B2DWT_L2_PREFETCH 0  // ring stages beyond the ring's own look-ahead prefetched into L2
+#endif
 
 // ---------------------------------------------------------------------------
 // Per-warp shared-memory ring.  One stage = RPS quad rows of 4*Q*32 elements,
@@ -732,6 +768,9 @@ struct RowSource {
         const int r0 = row0 + kk * RPS - a.in_row0;
         if constexpr (LIN == kLayoutInterleaved) {
           tma_load_3d(s, tm0, bar, 2 * m_strip, 2 * r0, b);
+          if constexpr (B2DWT_L2_PREFETCH > 0) {
+            if (kk + B2DWT_L2_PREFETCH < n_stages) tma_prefetch_3d(tm0, 2 * m_strip, 2 * (r0 + B2DWT_L2_PREFETCH * RPS), b);
+          }
         } else {
           constexpr int kPlane = RPS * Q * kLaneCount;
           tma_load_3d(s + 0 * kPlane, tm0, bar, m_strip, r0, b);
@@ -779,11 +818,14 @@ struct RowSource {
     ++k;
     const int g = base + k;
     if constexpr (kTma) {
+      // decided before the wait: under register pressure n_stages may live in
+      // local memory, and its load then overlaps the wait instead of following it
+      const bool refill = k + STAGES - 1 < n_stages;
 #ifndef B2DWT_EXPERIMENT_NOLOAD
-      mbar_wait(bars + (g % STAGES), (g / STAGES) & 1);
+      mbar_wait_keep(bars + (g % STAGES), (g / STAGES) & 1, refill);
 #endif
       __syncwarp();
-      if (k + STAGES - 1 < n_stages) {
+      if (refill) {
         if (lane == 0) fence_proxy_async();
         issue(k + STAGES - 1, a, tm0, tm1, tm2, tm3);
       }
@@ -886,6 +928,9 @@ __device__ __forceinline__ void steady_chunk(Pipe& pipe, Src& src, int t, const 
 //   kTma     fill the ring with TMA (requires 16 B pitches) instead of cp.async
 // f32: cap registers at 168/thread so 3 CTAs (12 warps) fit per SM; without
 // the hint ptxas spends ~200 and only 2 CTAs fit.
+#ifndef B2DWT_UNROLL
+#define B2DWT_UNROLL 1
+#endif
 #ifndef B2DWT_MIN_CTAS_PER_SM
 #define B2DWT_MIN_CTAS_PER_SM 3
 #endif
@@ -900,6 +945,10 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
   using Pipe = Stage<P, T, Q, kStrict, 0>;
   constexpr int kP = G::kPeriod;
   using Phases = std::make_integer_sequence<int, kP>;
+  // steady loop: B2DWT_UNROLL periods per iteration (more ticks in one basic
+  // block: the scheduler overlaps a tick's late stages with the next tick's early ones)
+  constexpr int kPS = kP * B2DWT_UNROLL;
+  using SteadyPhases = std::make_integer_sequence<int, kPS>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
 
   const int warp = threadIdx.x / kLaneCount;
@@ -1018,8 +1067,8 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
     // Run it entirely in the unchecked loop over whole periods: the extra fill
     // ticks before n0 compute rows outside the stored rows' cone (never read
     // by them), and the sink masks rows outside [n0, n1).
-    const int t_lo = (cx.first / kP) * kP;
-    const int t_hi = ((last_tick + kP) / kP) * kP;  // one past the last tick
+    const int t_lo = (cx.first / kPS) * kPS;
+    const int t_hi = ((last_tick + kPS) / kPS) * kPS;  // one past the last tick
     // (edge strips of narrow images need the generic column map: checked ticks only)
     const bool steady_ok = !hedge || cx.fold1;
     const bool unchecked = steady_ok && cx.n0 - G::up >= 0 && last_tick < a.rows && t_lo >= a.in_row0 &&
@@ -1047,9 +1096,9 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
     const int steady_hi = min(a.rows - 1, cx.n1 - 1 + G::down);
     int t = unchecked ? t_lo : cx.first;
     // first tick of the steady loop: >= steady_lo and a multiple of the period
-    const int s0 = unchecked ? t_lo : ((max(steady_lo, t) + kP - 1) / kP) * kP;
-    const bool has_steady = unchecked || (steady_ok && s0 + kP - 1 <= steady_hi);
-    const int s1 = unchecked ? t_hi : has_steady ? s0 + ((steady_hi - s0 + 1) / kP) * kP : s0;  // one past the steady ticks
+    const int s0 = unchecked ? t_lo : ((max(steady_lo, t) + kPS - 1) / kPS) * kPS;
+    const bool has_steady = unchecked || (steady_ok && s0 + kPS - 1 <= steady_hi);
+    const int s1 = unchecked ? t_hi : has_steady ? s0 + ((steady_hi - s0 + 1) / kPS) * kPS : s0;  // one past the steady ticks
     const int t_end = unchecked ? t_hi : last_tick + 1;
 #pragma unroll 1
     for (int round = 0; round < 2; ++round) {
@@ -1070,13 +1119,13 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
       if (round == 0 && has_steady) {
         if (hedge || sink.any_scalar) {
 #pragma unroll 1
-          for (; t < s1; t += kP)
-            steady_chunk<1, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, Phases{});
+          for (; t < s1; t += kPS)
+            steady_chunk<1, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, SteadyPhases{});
         } else {
           // interior strip: no halo folding, vector stores only
 #pragma unroll 1
-          for (; t < s1; t += kP)
-            steady_chunk<0, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, Phases{});
+          for (; t < s1; t += kPS)
+            steady_chunk<0, T, Q>(pipe, src, t, cx, a, sink, &tmap0, &tmap1, &tmap2, &tmap3, SteadyPhases{});
         }
       }
       if (!has_steady) break;

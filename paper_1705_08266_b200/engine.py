@@ -268,6 +268,42 @@ def _ptr(t) -> int:
     return int(t.data_ptr())
 
 
+def _check_buffer(torch, t, name, shape, dtype, device=None, host=False):
+    """Validate a caller-supplied buffer before its pointer reaches the C ABI:
+    a tensor of ``dtype`` and exactly ``shape``, on ``device`` (CUDA) or on the
+    host, with unit element stride and non-overlapping rows (and batch items).
+    A wrong buffer would otherwise become out-of-bounds device writes, or host
+    corruption through the pipelines' 2-D copies."""
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if host:
+        if t.device.type != "cpu":
+            raise ValueError(f"{name} must be a host (CPU) tensor")
+    elif not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    elif device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.numel() == 0:
+        return t
+    if t.stride(-1) != 1:
+        raise ValueError(f"{name} rows must be contiguous")
+    if t.dim() >= 2 and t.stride(-2) < t.shape[-1]:
+        raise ValueError(f"{name} rows overlap (row stride {t.stride(-2)} < {t.shape[-1]})")
+    if t.dim() == 3 and t.shape[0] > 1 and t.stride(0) < t.shape[1] * t.stride(1):
+        raise ValueError(f"{name} batch items overlap")
+    return t
+
+
+def _same_batch_stride(planes, name):
+    """The C ABI takes one batch stride for all four planes."""
+    if planes[0].shape[0] > 1 and any(p.stride(0) != planes[0].stride(0) for p in planes[1:]):
+        raise ValueError(f"{name}: the four planes must share one batch stride")
+
+
 class Transform:
     """Device-resident transform for one scheme at one precision.
 
@@ -277,7 +313,7 @@ class Transform:
     """
 
     def __init__(self, scheme, precision: str = "single", fast: bool = False, tma: bool = True,
-                 force_generic: bool = False, tile: bool | None = None):
+                 force_generic: bool = False, tile: bool | None = None, fuse: bool = True):
         self.scheme = scheme
         self.precision = precision
         self.np_dtype = np.dtype(PRECISION_DTYPES[precision])
@@ -289,6 +325,8 @@ class Transform:
             flags |= _native.FORCE_GENERIC
         if tile is not None:  # None: small levels tile, large ones stream
             flags |= _native.FORCE_TILE if tile else _native.NO_TILE
+        if not fuse:  # pyramids: one launch per level instead of fused level pairs
+            flags |= _native.NO_FUSE
         self.flags = flags
         self.fwd_program, self.inv_program = _programs(scheme)
         self.fwd_plan = plan_for(self.fwd_program, self.dtype, flags)
@@ -321,7 +359,7 @@ class Transform:
         if out is None:
             out = tuple(torch.empty((b, h // 2, w // 2), dtype=x.dtype, device=x.device) for _ in range(4))
         else:
-            out = tuple(o if o.dim() == 3 else o.unsqueeze(0) for o in out)
+            out = self._check_out_planes(torch, out, (b, h // 2, w // 2), x.device, batched)
         pl = _native.planes([_ptr(o) for o in out], [o.stride(1) for o in out], out[0].stride(0))
         _native.check(
             _native.load().b2dwt_forward(self.fwd_plan.handle, _ptr(xb), xb.stride(1), xb.stride(0), h, w, pl, b,
@@ -330,16 +368,46 @@ class Transform:
         )
         return out if batched else tuple(o[0] for o in out)
 
+    def _check_out_planes(self, torch, out, shape3, device, batched):
+        """Four caller-supplied output planes of ``shape3`` = (B, rows, cols)
+        (or (rows, cols) each for an unbatched call); returns 3-D views."""
+        if not isinstance(out, (tuple, list)) or len(out) != 4:
+            raise ValueError("out must be four planes (ll, hl, lh, hh)")
+        want = shape3 if batched else shape3[1:]
+        planes = []
+        for o, n in zip(out, ("ll", "hl", "lh", "hh")):
+            _check_buffer(torch, o, f"out[{n}]", want, self.torch_dtype, device)
+            planes.append(o if o.dim() == 3 else o.unsqueeze(0))
+        _same_batch_stride(planes, "out")
+        return tuple(planes)
+
+    def _check_in_planes(self, torch, comps, names):
+        """Four device input planes: same device, dtype, shape, contiguous rows
+        and one batch stride; returns 3-D views."""
+        first = comps[0]
+        self._check(first, names[0])
+        if first.dim() not in (2, 3):
+            raise ValueError(f"{names[0]} must be [rows, cols] or [B, rows, cols]")
+        for c, n in zip(comps[1:], names[1:]):
+            self._check(c, n)
+            if c.shape != first.shape:
+                raise ValueError("all four subbands must share dimensions")
+        planes = []
+        for c, n in zip(comps, names):
+            _check_buffer(torch, c, n, first.shape, self.torch_dtype, first.device)
+            planes.append(c if c.dim() == 3 else c.unsqueeze(0))
+        _same_batch_stride(planes, "subbands")
+        return planes
+
     def inverse(self, ll, hl, lh, hh, out=None, stream=None):
         torch = self._check(ll, "ll")
-        comps = [c if c.dim() == 3 else c.unsqueeze(0) for c in (ll, hl, lh, hh)]
-        shape = comps[0].shape
-        for c in comps[1:]:
-            if c.shape != shape:
-                raise ValueError("all four subbands must share dimensions")
-        b, rows, cols = shape
+        comps = self._check_in_planes(torch, (ll, hl, lh, hh), ("ll", "hl", "lh", "hh"))
+        b, rows, cols = comps[0].shape
         if out is None:
             out = torch.empty((b, 2 * rows, 2 * cols), dtype=ll.dtype, device=ll.device)
+        else:
+            _check_buffer(torch, out, "out", (b, 2 * rows, 2 * cols) if ll.dim() == 3 else (2 * rows, 2 * cols),
+                          self.torch_dtype, ll.device)
         ob = out if out.dim() == 3 else out.unsqueeze(0)
         pl = _native.planes([_ptr(c) for c in comps], [c.stride(1) for c in comps], comps[0].stride(0))
         _native.check(
@@ -352,10 +420,14 @@ class Transform:
     def run_components(self, comps, program=None, out=None, stream=None):
         torch = self._check(comps[0], "comps")
         plan = self.fwd_plan if program is None else plan_for(program, self.dtype, self.flags)
-        cs = [c if c.dim() == 3 else c.unsqueeze(0) for c in comps]
+        if len(comps) != 4:
+            raise ValueError("run_components takes four component planes")
+        cs = self._check_in_planes(torch, tuple(comps), tuple(f"comps[{i}]" for i in range(4)))
         b, rows, cols = cs[0].shape
         if out is None:
             out = [torch.empty_like(c) for c in cs]
+        else:
+            out = list(self._check_out_planes(torch, out, (b, rows, cols), comps[0].device, comps[0].dim() == 3))
         pin = _native.planes([_ptr(c) for c in cs], [c.stride(1) for c in cs], cs[0].stride(0))
         pout = _native.planes([_ptr(c) for c in out], [c.stride(1) for c in out], out[0].stride(0))
         _native.check(
@@ -370,10 +442,16 @@ class Transform:
         global_height x W image from a row band that starts at pixel row
         ``band_row0`` (must include the cone; see :attr:`cone`)."""
         torch = self._check(band, "band")
+        if band.dim() != 2:
+            raise ValueError("band must be [rows, W]")
         rows_b, w = band.shape
         n = out_row_end - out_row_begin
+        if n < 1:
+            raise ValueError("bad output row range")
         if out is None:
             out = tuple(torch.empty((n, w // 2), dtype=band.dtype, device=band.device) for _ in range(4))
+        else:
+            out = tuple(p[0] for p in self._check_out_planes(torch, out, (1, n, w // 2), band.device, False))
         pl = _native.planes([_ptr(o) for o in out], [o.stride(0) for o in out], 0)
         _native.check(
             _native.load().b2dwt_forward_rows(self.fwd_plan.handle, _ptr(band), band.stride(0), band_row0, rows_b,
@@ -382,6 +460,36 @@ class Transform:
             "forward_rows",
         )
         return out
+
+    def forward2(self, x, det0=None, out1=None, stream=None):
+        """Levels 0 and 1 of the pyramid of one ``[H, W]`` image in ONE kernel
+        (b2dwt_forward2): level 0's LL band never reaches HBM.  Returns
+        ``((hl0, lh0, hh0), (ll1, hl1, lh1, hh1))``, or ``None`` when the plan or
+        geometry does not fit the fused kernel (run two :meth:`forward` calls)."""
+        torch = self._check(x, "x")
+        if x.dim() != 2:
+            raise ValueError("forward2 takes one [H, W] image")
+        h, w = x.shape
+        if h % 4 or w % 4:
+            raise ValueError(f"dimensions must be divisible by 4, got {w}x{h}")
+        if det0 is None:
+            det0 = tuple(torch.empty((h // 2, w // 2), dtype=x.dtype, device=x.device) for _ in range(3))
+        if out1 is None:
+            out1 = tuple(torch.empty((h // 4, w // 4), dtype=x.dtype, device=x.device) for _ in range(4))
+        if len(det0) != 3 or len(out1) != 4:
+            raise ValueError("det0 holds (hl, lh, hh) and out1 (ll, hl, lh, hh)")
+        for b, n in zip(det0, ("hl", "lh", "hh")):
+            _check_buffer(torch, b, f"det0.{n}", (h // 2, w // 2), self.torch_dtype, x.device)
+        for b, n in zip(out1, ("ll", "hl", "lh", "hh")):
+            _check_buffer(torch, b, f"out1.{n}", (h // 4, w // 4), self.torch_dtype, x.device)
+        p0 = _native.planes([0] + [_ptr(b) for b in det0], [0] + [b.stride(0) for b in det0], 0)
+        p1 = _native.planes([_ptr(b) for b in out1], [b.stride(0) for b in out1], 0)
+        rc = _native.load().b2dwt_forward2(self.fwd_plan.handle, _ptr(x), x.stride(0), h, w, p0, p1,
+                                           _stream_handle(torch, stream))
+        if rc == _native.B2DWT_EUNSUPPORTED:
+            return None
+        _native.check(rc, "forward2")
+        return det0, out1
 
     @property
     def cone(self):
@@ -439,13 +547,38 @@ class Transform:
             cur = self.inverse(cur, hl, lh, hh, out=dst, stream=stream)
         return cur
 
+    def _check_pyramid(self, torch, h, w, levels, details, ll, device=None, host=False):
+        """Caller-supplied pyramid buffers: per level (hl, lh, hh) of
+        (H >> (l+1)) x (W >> (l+1)) and the final LL."""
+        if len(details) != levels:
+            raise ValueError(f"details must hold {levels} levels, got {len(details)}")
+        for lvl, d in enumerate(details):
+            if len(d) != 3:
+                raise ValueError("each level holds three detail planes (hl, lh, hh)")
+            for b, n in zip(d, ("hl", "lh", "hh")):
+                _check_buffer(torch, b, f"details[{lvl}].{n}", (h >> (lvl + 1), w >> (lvl + 1)), self.torch_dtype,
+                              device, host)
+        _check_buffer(torch, ll, "ll", (h >> levels, w >> levels), self.torch_dtype, device, host)
+
     def dwt_into(self, x, levels, details, ll, scratch, stream=None):
-        torch = _torch()
+        torch = self._check(x, "x")
+        if x.dim() != 2:
+            raise ValueError("dwt_into takes one [H, W] image")
+        h, w = x.shape
+        if levels < 1:
+            raise ValueError("levels must be >= 1")
+        if h % (1 << levels) or w % (1 << levels):
+            raise ValueError(f"dimensions must be divisible by 2^{levels}, got {w}x{h}")
+        self._check_pyramid(torch, h, w, levels, details, ll, x.device)
+        if levels > 1:
+            need = (h // 2) * (w // 2) + (h // 4) * (w // 4)
+            if scratch is None or not scratch.is_cuda or scratch.device != x.device or \
+                    scratch.dtype != self.torch_dtype or not scratch.is_contiguous() or scratch.numel() < need:
+                raise ValueError(f"scratch must be a contiguous {self.torch_dtype} device buffer of >= {need} elements")
         arr = (_native.Planes * levels)()
         for lvl, (hl, lh, hh) in enumerate(details):
             arr[lvl] = _native.planes([0, _ptr(hl), _ptr(lh), _ptr(hh)],
                                       [0, hl.stride(0), lh.stride(0), hh.stride(0)], 0)
-        h, w = x.shape
         _native.check(
             _native.load().b2dwt_dwt(self.fwd_plan.handle, _ptr(x), x.stride(0), h, w, levels, arr, _ptr(ll),
                                      ll.stride(0), _ptr(scratch) if scratch is not None else None,
@@ -483,14 +616,12 @@ class Transform:
                              for _ in range(3)) for l in range(levels)]
         if ll is None:
             ll = torch.empty((h >> levels, w >> levels), dtype=x.dtype, pin_memory=pin)
+        self._check_pyramid(torch, h, w, levels, details, ll, host=True)
         lib = _native.load()
         need = int(lib.b2dwt_dwt_host_workspace(self.fwd_plan.handle, h, w, levels))
         if need < 0:
             raise ValueError("bad dwt_host geometry")
-        ws = getattr(self, "_host_ws", None)
-        if ws is None or ws.numel() < need:
-            ws = torch.empty((need,), dtype=torch.uint8, device="cuda")
-            self._host_ws = ws
+        ws = _call_workspace(torch, need, stream)
         arr = (_native.Planes * levels)()
         for lvl, (hl, lh, hh) in enumerate(details):
             arr[lvl] = _native.planes([0, _ptr(hl), _ptr(lh), _ptr(hh)],
@@ -516,9 +647,16 @@ class Transform:
         if ll.dim() == 3:
             return self._idwt_batch(ll, details, out, stream)
         levels = len(details)
+        if levels < 1:
+            raise ValueError("levels must be >= 1")
+        if ll.dim() != 2:
+            raise ValueError("ll must be [rows, cols] or [B, rows, cols]")
         h, w = ll.shape[0] << levels, ll.shape[1] << levels
+        self._check_pyramid(torch, h, w, levels, details, ll, ll.device)
         if out is None:
             out = torch.empty((h, w), dtype=ll.dtype, device=ll.device)
+        else:
+            _check_buffer(torch, out, "out", (h, w), self.torch_dtype, ll.device)
         scratch = torch.empty(((h // 2) * (w // 2) + (h // 4) * (w // 4),), dtype=ll.dtype, device=ll.device) \
             if levels > 1 else None
         arr = (_native.Planes * levels)()
@@ -561,14 +699,12 @@ class Transform:
                     raise ValueError("all four subbands must share dimensions")
         if out is None:
             out = torch.empty((h, w), dtype=ll.dtype, pin_memory=ll.is_pinned())
+        _check_buffer(torch, out, "out", (h, w), self.torch_dtype, host=True)
         lib = _native.load()
         need = int(lib.b2dwt_idwt_host_workspace(self.inv_plan.handle, h, w, levels))
         if need < 0:
             raise ValueError("bad idwt_host geometry")
-        ws = getattr(self, "_host_iws", None)
-        if ws is None or ws.numel() < need:
-            ws = torch.empty((need,), dtype=torch.uint8, device="cuda")
-            self._host_iws = ws
+        ws = _call_workspace(torch, need, stream)
         arr = (_native.Planes * levels)()
         for lvl, (hl, lh, hh) in enumerate(details):
             arr[lvl] = _native.planes([0, _ptr(hl), _ptr(lh), _ptr(hh)],
@@ -600,6 +736,10 @@ class Transform:
             raise ValueError(f"dimensions must be even, got {w}x{h}")
         if out is None:
             out = tuple(torch.empty((b, h // 2, w // 2), dtype=x.dtype, pin_memory=x.is_pinned()) for _ in range(4))
+        if not isinstance(out, (tuple, list)) or len(out) != 4:
+            raise ValueError("out must be four planes (ll, hl, lh, hh)")
+        for o, n in zip(out, ("ll", "hl", "lh", "hh")):
+            _check_buffer(torch, o, f"out[{n}]", (b, h // 2, w // 2), self.torch_dtype, host=True)
         chunk = max(1, min(chunk, b))
         dev_in = [torch.empty((chunk, h, w), dtype=x.dtype, device="cuda") for _ in range(2)]
         dev_out = [torch.empty((4, chunk, h // 2, w // 2), dtype=x.dtype, device="cuda") for _ in range(2)]
@@ -636,11 +776,21 @@ class Transform:
         """Image rows [2*out_row_begin, 2*out_row_end) of the inverse from a row
         band of the four subband planes (quad rows [band_row0, band_row0 +
         rows)); mirror of :meth:`forward_rows` (b2dwt_inverse_rows)."""
-        torch = _torch()
+        torch = _require_cuda()
+        if len(band) != 4:
+            raise ValueError("band must be the four subband planes")
+        for b in band:
+            if b.dim() != 2:
+                raise ValueError("band planes must be [rows, cols]")
+        band = [p[0] for p in self._check_in_planes(torch, tuple(band), ("ll", "hl", "lh", "hh"))]
         ll = band[0]
         w = 2 * ll.shape[1]
+        if out_row_end <= out_row_begin:
+            raise ValueError("bad output row range")
         if out is None:
             out = torch.empty((2 * (out_row_end - out_row_begin), w), dtype=ll.dtype, device=ll.device)
+        else:
+            _check_buffer(torch, out, "out", (2 * (out_row_end - out_row_begin), w), self.torch_dtype, ll.device)
         pin = _native.planes([_ptr(b) for b in band], [b.stride(0) for b in band], 0)
         _native.check(
             _native.load().b2dwt_inverse_rows(self.inv_plan.handle, pin, band_row0, ll.shape[0], _ptr(out),
@@ -679,7 +829,9 @@ class PyramidGraph:
             else:
                 off = 0 if lvl % 2 == 0 else half
                 self._ll_views.append(self.scratch[off:off + hh_ * ww_].view(hh_, ww_))
-        self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(levels + 1)] \
+        # launch groups: the levels b2dwt_dwt runs in one kernel (fused pairs)
+        self.groups = self._groups(tr)
+        self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(self.groups) + 1)] \
             if level_events else None
         self._run(tr)
         torch.cuda.synchronize()
@@ -687,35 +839,80 @@ class PyramidGraph:
         with torch.cuda.graph(self.graph):
             self._run(tr)
 
+    def _groups(self, tr):
+        """[(first level, last level)] in launch order, as b2dwt_dwt groups them."""
+        groups, lvl = [], 0
+        while lvl < self.levels:
+            if lvl + 1 < self.levels:
+                src = self.x if lvl == 0 else self._ll_views[lvl - 1]
+                if tr.forward2(src, self.details[lvl], (self._ll_views[lvl + 1],) + tuple(self.details[lvl + 1])) \
+                        is not None:
+                    groups.append((lvl, lvl + 1))
+                    lvl += 2
+                    continue
+            groups.append((lvl, lvl))
+            lvl += 1
+        return groups
+
     def _run(self, tr):
-        src = self.x
-        for lvl in range(self.levels):
-            if self.events is not None:
-                self.events[lvl].record()
-            hl, lh, hh = self.details[lvl]
-            tr.forward(src, out=(self._ll_views[lvl], hl, lh, hh))
-            src = self._ll_views[lvl]
-        if self.events is not None:
-            self.events[self.levels].record()
+        if self.events is None:
+            # the product path: one b2dwt_dwt call (fused level pairs, PDL-chained)
+            tr.dwt_into(self.x, self.levels, self.details, self.ll, self.scratch)
+            return
+        for i, (a, b) in enumerate(self.groups):
+            self.events[i].record()
+            src = self.x if a == 0 else self._ll_views[a - 1]
+            if a == b:
+                hl, lh, hh = self.details[a]
+                tr.forward(src, out=(self._ll_views[a], hl, lh, hh))
+            else:
+                tr.forward2(src, self.details[a], (self._ll_views[b],) + tuple(self.details[b]))
+        self.events[len(self.groups)].record()
 
     def replay(self):
         self.graph.replay()
         return self.ll, self.details
 
     def level_ms(self):
-        """Kernel time of each level in the last replay (needs level_events=True)."""
-        return [self.events[i].elapsed_time(self.events[i + 1]) for i in range(self.levels)]
+        """Kernel time of each launch group (:attr:`groups`: a level, or a fused
+        pair of levels) in the last replay (needs level_events=True)."""
+        return [self.events[i].elapsed_time(self.events[i + 1]) for i in range(len(self.groups))]
 
 
-_TRANSFORMS: dict = {}
+def _call_workspace(torch, nbytes, stream):
+    """Device workspace for one host-pipeline call, from torch's caching
+    allocator on the call's stream: calls on different streams never share it,
+    and the block is recycled only after the stream has passed the call (the
+    library joins its internal copy streams back to that stream)."""
+    if stream is None:
+        return torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
+    with torch.cuda.stream(stream):
+        return torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
+
+
+_TRANSFORMS: "OrderedDict" = None
+_TRANSFORMS_MAX = 16
 
 
 def _transform(scheme, precision: str) -> Transform:
-    key = (id(scheme), precision)
+    """Transform for the reference-shaped API, cached by the compiled programs
+    (not the scheme object's identity: callers that rebuild the scheme per call
+    reuse one entry) in a small LRU; entries hold no device workspace."""
+    global _TRANSFORMS
+    from collections import OrderedDict
+
+    if _TRANSFORMS is None:
+        _TRANSFORMS = OrderedDict()
+    fwd, inv = _programs(scheme)
+    key = (_signature(fwd), _signature(inv), precision)
     t = _TRANSFORMS.get(key)
-    if t is None or t.scheme is not scheme:
+    if t is None:
         t = Transform(scheme, precision)
         _TRANSFORMS[key] = t
+        while len(_TRANSFORMS) > _TRANSFORMS_MAX:
+            _TRANSFORMS.popitem(last=False)
+    else:
+        _TRANSFORMS.move_to_end(key)
     return t
 
 

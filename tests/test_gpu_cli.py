@@ -58,10 +58,13 @@ def test_bench_writes_reference_csv(tmp_path):
     path = tmp_path / "b.csv"
     assert main(["bench", "--sizes", "64,256", "--reps", "5", "--csv", str(path)]) == EXIT_OK
     rows = list(csv.reader(open(path)))
-    assert tuple(rows[0]) == ("wavelet", "scheme", "width", "height", "precision", "threads", "tile", "reps",
-                              "median_seconds", "gbps")
+    # the reference's ten columns first (liftfuse/bench.py:22-33), then the GPU fields
+    assert tuple(rows[0][:10]) == ("wavelet", "scheme", "width", "height", "precision", "threads", "tile", "reps",
+                                   "median_seconds", "gbps")
+    assert tuple(rows[0][10:]) == ("device", "ngpu", "levels", "gpix_per_s", "roofline_frac")
     assert len(rows) == 1 + 2 * 4
-    assert all(float(r[-1]) > 0 for r in rows[1:])
+    assert all(float(r[9]) > 0 and float(r[13]) > 0 and float(r[14]) > 0 for r in rows[1:])
+    assert all("B200" in r[10] or r[10] for r in rows[1:])
 
 
 def test_read_raw_device(tmp_path):

@@ -6,9 +6,11 @@
 * C4 (1024 x 2048^2, batch): batched launches (footprint-split into chunks)
   equal per-image launches bit for bit on a sample of items, and items match
   the oracle;
-* C5 (65536^2): size-independent properties -- row bands computed from band
-  buffers (the multi-GPU strip building block) equal the whole-image transform
-  bit for bit, and forward + inverse reconstructs within 1e-4 x range.
+* C5 (65536^2): row bands computed from band buffers (the multi-GPU strip
+  building block) equal the whole-image transform bit for bit; the fast
+  whole-image output matches the f64 oracle on ~4100 x 65536 band buffers at
+  both global edges and in the interior; forward + inverse reconstructs within
+  1e-4 x range.
 """
 
 import numpy as np
@@ -64,6 +66,14 @@ def test_c4_batch_equals_items_and_oracle():
         got = strict.forward(x[b].contiguous())
         for g, w in zip(got, want):
             assert np.array_equal(g.cpu().numpy(), w), b
+    # the benchmarked (fast, FMA) batched outputs against the f64 oracle
+    for b in (5, 1000):
+        img = x[b].cpu().numpy()
+        want = oracle.forward(img.astype(np.float64), compile_scheme(SCHEME))
+        tol = 1e-4 * float(img.max() - img.min())
+        for c, w in zip(outs, want):
+            err = float(np.abs(c[b].cpu().numpy().astype(np.float64) - w).max())
+            assert err <= tol, (b, err)
 
 
 def test_c5_row_bands_and_round_trip():
@@ -81,6 +91,21 @@ def test_c5_row_bands_and_round_trip():
         out = tr.forward_rows(x[2 * b0:2 * b1], 2 * b0, n, r0, r1)
         for o, f in zip(out, full):
             assert torch.equal(o, f[r0:r1]), (r0, r1)
+    # fast bands against the f64 oracle run on a band buffer (~4100 x 65536):
+    # both global edges and one interior band.  The oracle reflects at the
+    # buffer's own cut edges too, which reaches at most `up`/`down` quad rows
+    # in from a cut, so the compared rows keep that margin from every cut.
+    prog = compile_scheme(SCHEME)
+    margin = 4
+    for r0, r1 in ((0, 2048), (rows // 2 - 1024, rows // 2 + 1024), (rows - 2048, rows)):
+        b0, b1 = max(0, r0 - up - margin), min(rows, r1 + down + margin)
+        band = x[2 * b0:2 * b1].cpu().numpy()
+        want = oracle.forward(band.astype(np.float64), prog)
+        tol = 1e-4 * float(band.max() - band.min())
+        for c, w in zip(full, want):
+            err = float(np.abs(c[r0:r1].cpu().numpy().astype(np.float64) - w[r0 - b0:r1 - b0]).max())
+            assert err <= tol, (r0, r1, err)
+        del band, want
     rec = tr.inverse(*full)
     del full
     err = 0.0
