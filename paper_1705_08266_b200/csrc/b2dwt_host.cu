@@ -446,11 +446,17 @@ cudaError_t launch_gtile(const b2dwt_plan_s& p, const GTileProgram& g, const Fus
   if (e != cudaSuccess) return e;
   e = cudaMemcpyAsync(dg, &g, sizeof(GTileProgram), cudaMemcpyHostToDevice, r.stream);
   if (e == cudaSuccess) {
-    // opt in to the large dynamic shared memory once per instantiation
-    static const cudaError_t attr_strict = cudaFuncSetAttribute(
-        generic_tile_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    static const cudaError_t attr_fast = cudaFuncSetAttribute(
-        generic_tile_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    // opt in to the large dynamic shared memory once per instantiation and device
+    static PerDevice once;
+    static cudaError_t attr[kMaxDevices][2] = {};
+    const int dev = once.run([&](int d) {
+      attr[d][0] = cudaFuncSetAttribute(generic_tile_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem));
+      attr[d][1] = cudaFuncSetAttribute(generic_tile_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem));
+    });
+    const cudaError_t attr_strict = dev < 0 ? cudaErrorNotSupported : attr[dev][0];
+    const cudaError_t attr_fast = dev < 0 ? cudaErrorNotSupported : attr[dev][1];
     if (strict_of(&p)) {
       e = attr_strict;
       if (e == cudaSuccess)
@@ -603,6 +609,21 @@ int64_t fuse2_min_quads() {
   return e ? std::atoll(e) : int64_t{1} << 20;
 }
 
+// Levels at which b2dwt_dwt may start a fused pair (greedy from level 0 by
+// default); B2DWT_FUSE2_PAIRS="0,3" e.g. pairs (0,1) and (3,4) only.
+bool fuse2_starts_at(int level) {
+  const char* e = std::getenv("B2DWT_FUSE2_PAIRS");
+  if (!e) return true;
+  for (const char* p = e; *p;) {
+    char* end = nullptr;
+    const long v = std::strtol(p, &end, 10);
+    if (end == p) break;
+    if (v == level) return true;
+    p = *end ? end + 1 : end;
+  }
+  return false;
+}
+
 // Levels l and l+1 of a forward pyramid in one kernel (fused2_kernel.cuh):
 // level l's LL never reaches HBM.  B2DWT_EUNSUPPORTED when the request does not
 // fit it (the caller then runs the two levels separately).
@@ -635,16 +656,21 @@ int run_fused2_pair(const b2dwt_plan_s& p, const void* in, int64_t in_ld, int64_
   // work split of the fused kernel: a unit re-reads the cones of BOTH levels
   // (~14 level-l rows), so its dynamic tail chunks are longer than the stream
   // kernel's.  B2DWT_F2_STATIC_FRAC / B2DWT_F2_TAIL_ROWS override.
-  static const int f2_static = [] {
+  static const int f2_static = [] {  // measured on C3 (tools/f2_sweep.sh): 896-928 best
     const char* e = std::getenv("B2DWT_F2_STATIC_FRAC");
-    return e ? std::atoi(e) : 832;
+    return e ? std::atoi(e) : 912;
   }();
   static const int f2_tail = [] {
     const char* e = std::getenv("B2DWT_F2_TAIL_ROWS");
-    return e ? std::atoi(e) : 48;
+    return e ? std::atoi(e) : 16;
+  }();
+  static const int f2_edge = [] {
+    const char* e = std::getenv("B2DWT_F2_EDGE_ROWS");
+    return e ? std::atoi(e) : 8;
   }();
   r.static_frac = f2_static;
   r.tail_rows1 = f2_tail;
+  r.edge_rows1 = f2_edge;
   r.min_rows1 = std::max(8, min_rows() / 2);
   r.pdl = split_param(4) != 0;
   r.stream = stream;
@@ -697,7 +723,8 @@ int check_dims(int64_t height, int64_t width) {
                   static_cast<long long>(height));
     return fail(B2DWT_EINVAL, buf);
   }
-  if (height / 2 > (1LL << 30) || width / 2 > (1LL << 30))
+  // the reflection map works in 32-bit pixel coordinates (period 4*cs - 2)
+  if (height / 2 > (1LL << 29) || width / 2 > (1LL << 29))
     return fail(B2DWT_EUNSUPPORTED, "image too large for 32-bit quad indexing");
   return B2DWT_OK;
 }
@@ -1038,11 +1065,16 @@ int b2dwt_dwt(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t heig
   if (scratch) sc[1] = sc[0] + static_cast<size_t>((height / 2) * (width / 2)) * es;
   const void* in = image;
   int64_t in_ld = image_ld;
+  int in_sc = -1;  // scratch half holding the current input (-1: the image)
+  // a level's LL (unless final) goes to the scratch half it does not read:
+  // level 0's to sc[0] (the only one large enough), later ones alternate
+  auto ll_half = [&](int level) { return in_sc == 0 ? 1 : in_sc == 1 ? 0 : (level == 0 ? 0 : 1); };
   for (int l = 0; l < levels; ++l) {
     const int64_t h = height >> l, w = width >> l;
-    if (l + 1 < levels) {
+    if (l + 1 < levels && fuse2_starts_at(l)) {
       // levels l and l+1 in one kernel when the plan and geometry allow it
-      void* ll1 = l + 1 == levels - 1 ? ll_out : sc[(l + 1) & 1];
+      const int half = ll_half(l + 1);
+      void* ll1 = l + 1 == levels - 1 ? ll_out : sc[half];
       const int64_t ll1_ld = l + 1 == levels - 1 ? ll_ld : w / 4;
       char name[40];
       std::snprintf(name, sizeof(name), "b2dwt dwt levels %d+%d", l, l + 1);
@@ -1052,6 +1084,7 @@ int b2dwt_dwt(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t heig
       if (rc == B2DWT_OK) {
         in = ll1;
         in_ld = ll1_ld;
+        in_sc = half;
         ++l;
         continue;
       }
@@ -1064,7 +1097,8 @@ int b2dwt_dwt(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t heig
       lv.ptr[0] = ll_out;
       lv.ld[0] = ll_ld;
     } else {
-      lv.ptr[0] = sc[l & 1];
+      in_sc = ll_half(l);
+      lv.ptr[0] = sc[in_sc];
       lv.ld[0] = w / 2;
     }
     char name[32];

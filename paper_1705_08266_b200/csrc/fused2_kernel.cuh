@@ -14,17 +14,20 @@
 //
 // Geometry (all built-in lifting programs: per-sub-step horizontal reach <= 1,
 // cone <= 2 quads per side):
-//   CTA super-strip c owns level-l quad columns [208c, 208c + 208) and level
-//   l+1 columns [104c, 104c + 104) (both whole 32-B sectors in f32).
-//   Level l:   warp w loads quads m0 + [0, 64), m0 = 208c - 8 + 56w (32-B
-//              aligned), keeps the LL of lanes 2..29 (quads m0 + [4, 60), inside
-//              its valid cone) and stores HL/LH/HH of its share of the CTA's
-//              columns (56-quad warp boundaries: whole sectors).
+//   CTA super-strip c owns level-l quad columns [224c, 224c + 224) and level
+//   l+1 columns [112c, 112c + 112) (both whole 32-B sectors in f32) -- the
+//   stream kernel's 256 loaded quads per 224 stored.
+//   Level l:   warp w loads quads m0 + [0, 64), m0 = 224c - 8 + 60w (32-B
+//              aligned); its valid lanes 1..30 (quads m0 + [2, 62)) publish
+//              their LL and store HL/LH/HH of the CTA's columns among them.
 //   Ring:      level-(l+1) quads: slot[j] = (c0, c1, c2, c3) of level-(l+1)
-//              column 104c - 2 + j, j in [0, 112); level-l lane l of warp w
-//              writes j = 28w + l - 2 (even LL row: c0/c1, odd row: c2/c3).
-//   Level l+1: warp w, lane l runs column 104c - 2 + 26w + l (Q = 1) and stores
-//              [104c + 26w, +26) (valid lanes are 2..29).
+//              column 112c - 2 + j, j in [0, 116); level-l lane l of warp w
+//              writes j = 30w + l - 2 (even LL row: c0/c1, odd row: c2/c3).
+//   Level l+1: warp w, lane l runs column 112c - 2 + 28w + l (Q = 1) and stores
+//              [112c + 28w, +28) (valid lanes are 2..29).
+// Warp boundaries inside a super-strip are not sector-aligned; the warps of a
+// CTA run in lockstep (below), so both halves of a shared sector reach L2
+// together.
 // Warp w reads ring columns of warps w-1 and w+1 and they read its columns, so
 // each warp signals one mbarrier per ring slot (32 arrivals) and waits only for
 // its neighbours' -- which also proves they are done reading the slot it is
@@ -44,15 +47,15 @@
 
 namespace b2dwt {
 
-constexpr int kF2SuperW = 208;  // level-l quads per CTA super-strip
-constexpr int kF2StripW = 56;   // level-l quads between the warps' strips
+constexpr int kF2SuperW = 224;  // level-l quads per CTA super-strip
+constexpr int kF2StripW = 60;   // level-l quads between the warps' strips
 constexpr int kF2Lead = 8;      // level-l quads loaded left of the CTA's columns
 #ifndef B2DWT_F2_RING
 #define B2DWT_F2_RING 6
 #endif
 constexpr int kF2Ring = B2DWT_F2_RING;  // ring slots (level-(l+1) rows)
-constexpr int kF2J = 112;               // ring columns (level-(l+1) quads)
-constexpr int kF2W1 = 26;               // level-(l+1) columns stored per warp
+constexpr int kF2J = 116;               // ring columns (level-(l+1) quads)
+constexpr int kF2W1 = 28;               // level-(l+1) columns stored per warp
 constexpr int kF2Edge = 8;      // level-(l+1) rows at the image top / bottom run as checked units
 
 template <class T>
@@ -77,31 +80,49 @@ struct Fused2Args {
   int n_ctas;
   unsigned long long* tail_counter;  // [0] tickets, [1] CTAs done (self-resetting), or null
   int tail_chunk;                    // level-(l+1) rows per dynamic chunk
-  // work space (f2_work_space on the host): interior rows [ki0, ki0 + rows_in)
-  // of every super-strip, unit cost = one level-(l+1) row; [0, static_end)
-  // split evenly over the CTAs; dynamic items = the `top` / `bot` edge units of
-  // every super-strip (n_edge), then tail chunks of [static_end, total)
-  int top, bot, ki0, rows_in, n_edge;
-  int total, static_end, n_dyn;
+  // work space (f2_work_space on the host), in cost units of one interior
+  // level-(l+1) row: [0, edge_cost) = the n_edge checked units of kF2Edge rows
+  // at the image top / bottom (`top` / `bot` rows per super-strip), each
+  // costing unit_cost; then [edge_cost, total) = interior rows [ki0, ki0 +
+  // rows_in) of every super-strip.  [static_begin, static_end) is split evenly
+  // over the CTAs (a unit goes to the CTA whose share holds its first cost
+  // unit); with a tail counter the edge units are the first dynamic items
+  // (dyn_edges) and the interior past static_end follows in tail chunks.
+  int top, bot, ki0, rows_in, n_edge, unit_cost, edge_cost;
+  int total, static_begin, static_end, dyn_edges, n_dyn;
 };
 
 // Host: fill the work-space fields of `a` (its k range, n_super, tail_counter,
 // tail_chunk and rows already set).  The rows within kF2Edge of the image top /
 // bottom need the checked (reflecting) path at both levels and run as short
-// separate units, so no long segment is ever checked.
+// separate units, so no long segment is ever checked; they sit at the head of
+// the static split, weighted by their cost (checked ticks plus both cones).
 template <class T>
-inline void f2_work_space(Fused2Args<T>& a, int static_frac) {
+inline void f2_work_space(Fused2Args<T>& a, int static_frac, int edge_rows = kF2Edge) {
   const int rows1 = a.rows / 2;
-  a.top = a.k_begin == 0 ? (a.k_end - a.k_begin < kF2Edge ? a.k_end - a.k_begin : kF2Edge) : 0;
+  const int edge = edge_rows < 1 ? 1 : edge_rows;
+  a.top = a.k_begin == 0 ? (a.k_end - a.k_begin < edge ? a.k_end - a.k_begin : edge) : 0;
   const int rest = a.k_end - a.k_begin - a.top;
-  a.bot = a.k_end == rows1 ? (rest < kF2Edge ? rest : kF2Edge) : 0;
+  a.bot = a.k_end == rows1 ? (rest < edge ? rest : edge) : 0;
   a.ki0 = a.k_begin + a.top;
   a.rows_in = a.k_end - a.bot - a.ki0;
   a.n_edge = (a.top > 0 ? a.n_super : 0) + (a.bot > 0 ? a.n_super : 0);
-  a.total = a.n_super * a.rows_in;
-  a.static_end = a.tail_counter != nullptr ? static_cast<int>(static_cast<int64_t>(a.total) * static_frac / 1024)
-                                           : a.total;
-  a.n_dyn = a.n_edge + (a.total - a.static_end + a.tail_chunk - 1) / a.tail_chunk;
+  a.unit_cost = 6 * edge;  // checked ticks at both levels plus both cones, per edge unit
+  a.edge_cost = a.n_edge * a.unit_cost;
+  a.total = a.edge_cost + a.n_super * a.rows_in;
+  if (a.tail_counter != nullptr) {
+    // large launch: the slow edge units go to whichever CTAs finish their
+    // static share first (head of the dynamic list)
+    a.static_begin = a.edge_cost;
+    a.static_end = a.edge_cost + static_cast<int>(static_cast<int64_t>(a.total - a.edge_cost) * static_frac / 1024);
+    a.dyn_edges = a.n_edge;
+  } else {
+    // small launch: everything static, edge units weighted into the split
+    a.static_begin = 0;
+    a.static_end = a.total;
+    a.dyn_edges = 0;
+  }
+  a.n_dyn = a.dyn_edges + (a.total - a.static_end + a.tail_chunk - 1) / a.tail_chunk;
 }
 
 // Level-l sink: HL/LH/HH straight to HBM (8-B vectors), LL into the ring.
@@ -333,30 +354,45 @@ __global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
 
   const int rows1 = a.rows / 2, cols1 = a.cols / 2;
   // work space: see Fused2Args / f2_work_space
-  int f = static_cast<int>(static_cast<int64_t>(a.static_end) * cta / a.n_ctas);
-  int f_end = static_cast<int>(static_cast<int64_t>(a.static_end) * (cta + 1) / a.n_ctas);
-  int item = cta;  // next dynamic item without a counter: round robin
+  const int64_t span = a.static_end - a.static_begin;
+  int f = a.static_begin + static_cast<int>(span * cta / a.n_ctas);
+  int f_end = a.static_begin + static_cast<int>(span * (cta + 1) / a.n_ctas);
 
   F2Level1<P, T, kStrict> l1;
   l1.bars = ll_bars;
   l1.warp = warp;
   l1.u = 0;
   l1.rd = ll_ring + static_cast<unsigned>((kF2W1 * warp + lane) * 4 * sizeof(T));
-  const unsigned ring_w =  // this lane's published column (lanes 2..29), or 0
-      lane >= 2 && lane < 30 ? ll_ring + static_cast<unsigned>((28 * warp + lane - 2) * 4 * sizeof(T)) : 0u;
+  const int jw = kF2StripW / 2 * warp + lane - 2;  // ring column of this lane's LL
+  const unsigned ring_w =                         // published by the valid lanes 1..30, or 0
+      lane >= 1 && lane <= 30 && jw >= 0 && jw < kF2J ? ll_ring + static_cast<unsigned>(jw * 4 * sizeof(T)) : 0u;
 
 #pragma unroll 1
   for (;;) {
     // next unit: super-strip `sup`, level-(l+1) rows [k0, k1) (CTA-uniform)
     int sup, k0, k1;
-    if (f < f_end) {  // static share: [f, f_end) of the interior cost space
-      sup = f / a.rows_in;
-      const int c0 = sup * a.rows_in;
-      k0 = a.ki0 + (f - c0);
-      k1 = a.ki0 + min(a.rows_in, f_end - c0);
-      f = c0 + a.rows_in;
-      if (k0 >= k1) continue;
-    } else {  // next dynamic item
+    if (f < f_end) {
+      if (f < a.edge_cost) {  // edge units: this CTA's if their first cost unit lies in [f, f_end)
+        const int e = (f + a.unit_cost - 1) / a.unit_cost;  // first unit starting at or after f
+        if (e >= a.n_edge || e * a.unit_cost >= f_end) {  // none: continue with the interior rows
+          f = min(a.edge_cost, f_end);
+          continue;
+        }
+        f = (e + 1) * a.unit_cost;
+        const bool is_top = a.top > 0 && e < a.n_super;
+        sup = is_top ? e : e - (a.top > 0 ? a.n_super : 0);
+        k0 = is_top ? a.k_begin : a.k_end - a.bot;
+        k1 = is_top ? a.k_begin + a.top : a.k_end;
+      } else {  // interior rows
+        const int g = f - a.edge_cost;
+        sup = g / a.rows_in;
+        const int c0 = sup * a.rows_in;
+        k0 = a.ki0 + (g - c0);
+        k1 = a.ki0 + min(a.rows_in, f_end - a.edge_cost - c0);
+        f = a.edge_cost + c0 + a.rows_in;
+        if (k0 >= k1) continue;
+      }
+    } else {  // next dynamic tail chunk (interior rows)
       int j;
       if (a.tail_counter != nullptr) {
         __syncthreads();
@@ -364,19 +400,17 @@ __global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
         __syncthreads();
         j = static_cast<int>(min(s_ticket, static_cast<unsigned long long>(a.n_dyn)));
       } else {
-        j = item;
-        item += a.n_ctas;
+        j = a.n_dyn;
       }
       if (j >= a.n_dyn) break;
-      if (j >= a.n_edge) {
-        f = a.static_end + (j - a.n_edge) * a.tail_chunk;
+      if (j < a.dyn_edges) {  // edge unit j: its cost range, taken whole by this CTA
+        f = j * a.unit_cost;
+        f_end = f + 1;
+      } else {
+        f = a.static_end + (j - a.dyn_edges) * a.tail_chunk;
         f_end = min(a.total, f + a.tail_chunk);
-        continue;
       }
-      const bool is_top = a.top > 0 && j < a.n_super;
-      sup = is_top ? j : j - (a.top > 0 ? a.n_super : 0);
-      k0 = is_top ? a.k_begin : a.k_end - a.bot;
-      k1 = is_top ? a.k_begin + a.top : a.k_end;
+      continue;
     }
     // level l: valid LL rows [n0p, n1p), HL/LH/HH rows [2 k0, 2 k1) stored
     const int n0p = max(0, 2 * (k0 - G::up));
@@ -424,7 +458,7 @@ __global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
     F2Sink0<T> sink0;
     {
       const int own0 = kF2SuperW * sup, own1 = min(a.cols, own0 + kF2SuperW);
-      const int w0 = cx.m_strip + 4, w1 = cx.m_strip + 60;  // this warp's published LL columns
+      const int w0 = cx.m_strip + 2, w1 = cx.m_strip + 62;  // this warp's valid columns (lanes 1..30)
       sink0.init(a, cx.m_lane, max(own0, w0), min(own1, w1));
       sink0.ring = ring_w;
       sink0.slot = static_cast<int>(l1.u % kF2Ring);

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 namespace b2dwt {
 
 struct FusedLaunch {
@@ -61,9 +63,29 @@ struct Fused2Launch {
   unsigned long long* tail_counter;
   int static_frac;
   int tail_rows1;
+  int edge_rows1;  // level-(l+1) rows per checked unit at the image top / bottom
   int min_rows1;
   bool pdl;
   cudaStream_t stream;
+};
+
+// One-time setup per device (function attributes and occupancy are per
+// device): run(f) calls f(device) the first time it is reached on each device.
+constexpr int kMaxDevices = 64;
+struct PerDevice {
+  std::mutex mu;
+  bool done[kMaxDevices] = {};
+  template <class F>
+  int run(F&& f) {  // the current device, or -1
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return -1;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!done[dev]) {
+      f(dev);
+      done[dev] = true;
+    }
+    return dev;
+  }
 };
 
 // RAII NVTX range (b2dwt_host.cu); a no-op unless B2DWT_NVTX is set.

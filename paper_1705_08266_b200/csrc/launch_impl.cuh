@@ -86,15 +86,13 @@ bool make_map(CUtensorMap* map, const void* base, int64_t width, int64_t height,
 }
 
 int num_sms() {
-  static int sms = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+  static PerDevice once;
+  static int sms[kMaxDevices] = {};
+  const int dev = once.run([](int d) {
+    cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, d);
+    if (sms[d] <= 0) sms[d] = 148;
   });
-  return sms;
+  return dev < 0 ? 148 : sms[dev];
 }
 
 template <class Prog, class T, int LIN, int LOUT, bool kStrict, bool kTma>
@@ -106,13 +104,15 @@ cudaError_t launch(const FusedLaunch& r) {
   constexpr size_t kRing = static_cast<size_t>(kWarps) * kStages * kRps * RowGeom<T, kQ>::kBytes;
   constexpr size_t kSmem = kRing + (kTma ? kWarps * kStages * sizeof(uint64_t) : 0);
 
-  static int blocks_per_sm = 0;
-  static std::once_flag once;
-  std::call_once(once, [&] {
+  static PerDevice once;
+  static int bps[kMaxDevices] = {};
+  const int dev = once.run([&](int d) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kWarps * kLaneCount, kSmem);
-    if (blocks_per_sm <= 0) blocks_per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps[d], kern, kWarps * kLaneCount, kSmem);
+    if (bps[d] <= 0) bps[d] = 1;
   });
+  if (dev < 0) return cudaErrorNotSupported;
+  const int blocks_per_sm = bps[dev];
 
   Args a{};
   a.in_img = static_cast<const T*>(r.in_img);

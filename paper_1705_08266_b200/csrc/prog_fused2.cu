@@ -57,26 +57,18 @@ cudaError_t launch(const Fused2Launch& r) {
   constexpr size_t kSmem = kRing0 + 4 * kStages * sizeof(uint64_t) + kF2Ring * kF2J * 4 * sizeof(T) +
                            kF2Ring * 4 * sizeof(uint64_t);
   // per device: the smem opt-in and occupancy (attributes are per device)
-  constexpr int kMaxDev = 64;
-  static KernelInfo<kStrict> info[kMaxDev];
-  static std::mutex mu;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return cudaErrorNotSupported;
-  KernelInfo<kStrict> ki;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    if (info[dev].sms == 0) {
-      KernelInfo<kStrict> k;
-      k.attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
-      if (k.attr == cudaSuccess)
-        k.attr = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k.blocks_per_sm, kern, 128, kSmem);
-      cudaDeviceGetAttribute(&k.sms, cudaDevAttrMultiProcessorCount, dev);
-      if (k.sms <= 0) k.sms = 148;
-      if (k.blocks_per_sm <= 0) k.blocks_per_sm = 1;
-      info[dev] = k;
-    }
-    ki = info[dev];
-  }
+  static PerDevice once;
+  static KernelInfo<kStrict> info[kMaxDevices];
+  const int dev = once.run([&](int d) {
+    KernelInfo<kStrict>& k = info[d];
+    k.attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
+    if (k.attr == cudaSuccess) k.attr = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k.blocks_per_sm, kern, 128, kSmem);
+    cudaDeviceGetAttribute(&k.sms, cudaDevAttrMultiProcessorCount, d);
+    if (k.sms <= 0) k.sms = 148;
+    if (k.blocks_per_sm <= 0) k.blocks_per_sm = 1;
+  });
+  if (dev < 0) return cudaErrorNotSupported;
+  const KernelInfo<kStrict> ki = info[dev];
   if (ki.attr != cudaSuccess) return ki.attr;
 
   Fused2Args<T> a{};
@@ -104,7 +96,7 @@ cudaError_t launch(const Fused2Launch& r) {
   const int64_t per_cta = total / a.n_ctas;
   a.tail_counter = per_cta >= 64 ? r.tail_counter : nullptr;
   a.tail_chunk = static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(r.tail_rows1, per_cta / 4)));
-  f2_work_space(a, std::min(1024, std::max(0, r.static_frac)));
+  f2_work_space(a, std::min(1024, std::max(0, r.static_frac)), r.edge_rows1);
 
   EncodeTiledFn enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;

@@ -23,12 +23,13 @@ cudaError_t launch_tile_wr(const FusedLaunch& r) {
   using TG = TileGeo<P, WR>;
   auto kern = tile_kernel<P, T, kMainIn, kMainOut, kStrict, WR>;
   constexpr size_t kSmem = tile_smem_bytes<P, T, WR>();
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
+  static PerDevice once;
+  static cudaError_t attr_err[kMaxDevices] = {};
+  const int dev = once.run([&](int d) {
+    attr_err[d] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
   });
-  if (attr_err != cudaSuccess) return attr_err;
+  if (dev < 0) return cudaErrorNotSupported;
+  if (attr_err[dev] != cudaSuccess) return attr_err[dev];
   TileArgs<T> a{};
   a.in_img = static_cast<const T*>(r.in_img);
   for (int c = 0; c < 4; ++c) {

@@ -819,18 +819,21 @@ class PyramidGraph:
         self.ll, self.details = tr.dwt(x, levels)  # allocates + warms up every level
         self.scratch = torch.empty(((h // 2) * (w // 2) + (h // 4) * (w // 4),), dtype=x.dtype, device=x.device) \
             if levels > 1 else None
-        # per-level output views: level l writes LL into scratch (or the final ll)
-        half = (h // 2) * (w // 2)
-        self._ll_views = []
-        for lvl in range(levels):
-            hh_, ww_ = h >> (lvl + 1), w >> (lvl + 1)
-            if lvl == levels - 1:
-                self._ll_views.append(self.ll)
-            else:
-                off = 0 if lvl % 2 == 0 else half
-                self._ll_views.append(self.scratch[off:off + hh_ * ww_].view(hh_, ww_))
-        # launch groups: the levels b2dwt_dwt runs in one kernel (fused pairs)
+        # launch groups: the levels b2dwt_dwt runs in one kernel (fused pairs),
+        # and where each group's LL lands: the scratch half it does not read
+        # (b2dwt_host.cu b2dwt_dwt), the final one in ``ll``
         self.groups = self._groups(tr)
+        half = (h // 2) * (w // 2)
+        self._ll_views = [None] * levels
+        in_sc = -1
+        for a, b in self.groups:
+            hh_, ww_ = h >> (b + 1), w >> (b + 1)
+            if b == levels - 1:
+                self._ll_views[b] = self.ll
+                continue
+            in_sc = 1 if in_sc == 0 else 0 if in_sc == 1 else (0 if b == 0 else 1)
+            off = 0 if in_sc == 0 else half
+            self._ll_views[b] = self.scratch[off:off + hh_ * ww_].view(hh_, ww_)
         self.events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(self.groups) + 1)] \
             if level_events else None
         self._run(tr)
@@ -840,16 +843,28 @@ class PyramidGraph:
             self._run(tr)
 
     def _groups(self, tr):
-        """[(first level, last level)] in launch order, as b2dwt_dwt groups them."""
+        """[(first level, last level)] in launch order, as b2dwt_dwt groups them
+        (b2dwt_host.cu: a pair starts where B2DWT_FUSE2_PAIRS allows, on levels of
+        at least B2DWT_FUSE2_MIN_QUADS quads, when the fused kernel takes it)."""
+        import os
+
+        min_quads = int(os.environ.get("B2DWT_FUSE2_MIN_QUADS", 1 << 20))
+        starts = os.environ.get("B2DWT_FUSE2_PAIRS")
+        starts = None if starts is None else {int(v) for v in starts.split(",") if v.strip()}
+        h, w = self.x.shape
+        torch = _torch()
+        # does the plan have a fused kernel at all? (a tiny probe; geometry below)
+        probe = torch.zeros((16, 256), dtype=self.x.dtype, device=self.x.device)
+        fusable = not (tr.flags & _native.NO_FUSE) and tr.forward2(probe) is not None
         groups, lvl = [], 0
         while lvl < self.levels:
-            if lvl + 1 < self.levels:
-                src = self.x if lvl == 0 else self._ll_views[lvl - 1]
-                if tr.forward2(src, self.details[lvl], (self._ll_views[lvl + 1],) + tuple(self.details[lvl + 1])) \
-                        is not None:
-                    groups.append((lvl, lvl + 1))
-                    lvl += 2
-                    continue
+            hl, wl = h >> lvl, w >> lvl
+            if fusable and lvl + 1 < self.levels and min_quads > 0 and (hl // 2) * (wl // 2) >= min_quads \
+                    and (starts is None or lvl in starts) and hl % 4 == 0 and wl % 4 == 0 and wl >= 256 \
+                    and (self.x.stride(0) * self.x.element_size()) % 16 == 0:
+                groups.append((lvl, lvl + 1))
+                lvl += 2
+                continue
             groups.append((lvl, lvl))
             lvl += 1
         return groups

@@ -87,6 +87,37 @@ def test_fused_footprint_bands_padded_pitch_and_dynamic_tail(monkeypatch):
         assert torch.equal(g, wv)
 
 
+@pytest.mark.parametrize("fast", [False, True], ids=["strict", "fast"])
+def test_two_fused_pairs_in_one_pyramid(fast, monkeypatch):
+    """5 levels = pairs (0,1) and (2,3) plus level 4: the second pair reads one
+    scratch half and must write its LL into the other (b2dwt_dwt), also inside
+    the captured graph and its per-group event variant."""
+    monkeypatch.setenv("B2DWT_FUSE2_MIN_QUADS", "1")
+    s = build_scheme("non-separable-split", CDF97)
+    img = np.random.default_rng(2).random((1024, 1536)).astype(np.float32)
+    x = torch.from_numpy(img).cuda()
+    fused = Transform(s, "single", fast=fast)
+    plain = Transform(s, "single", fast=fast, fuse=False)
+    a_ll, a_det = fused.dwt(x, 5)
+    b_ll, b_det = plain.dwt(x, 5)
+    assert torch.equal(a_ll, b_ll)
+    for lvl in range(5):
+        for u, v in zip(a_det[lvl], b_det[lvl]):
+            assert torch.equal(u, v), lvl
+    for events in (False, True):
+        g = fused.capture_dwt(x, 5, level_events=events)
+        assert g.groups == [(0, 1), (2, 3), (4, 4)]
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(g.ll, b_ll), events
+        for lvl in range(5):
+            for u, v in zip(g.details[lvl], b_det[lvl]):
+                assert torch.equal(u, v), (events, lvl)
+    if not fast:
+        want_ll, _ = oracle.dwt(img, compile_scheme(s), 5)
+        assert np.array_equal(a_ll.cpu().numpy(), want_ll)
+
+
 def test_unfusable_requests_fall_back():
     s = build_scheme("separable-convolution", CDF97)  # per-sub-step reach 2: no fused kernel
     tr = Transform(s, "single")
