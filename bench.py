@@ -322,9 +322,9 @@ def _launches(rows, cols, batch=1, levels=1):
 
 def _c3_launches(groups, n):
     """Kernel launches of one C3 pyramid: a fused level pair runs as row bands of
-    <= 512 MiB of level-l input (b2dwt_host.cu run_fused2_pair), a single level
+    <= 1 GiB of level-l input (b2dwt_host.cu run_fused2_pair), a single level
     as _launches counts it."""
-    cap = int(os.environ.get("B2DWT_MAX_LAUNCH_BYTES", 512 << 20))
+    cap = int(os.environ.get("B2DWT_F2_MAX_LAUNCH_BYTES", 1 << 30))
     total = 0
     for a, b in groups:
         r = n >> (a + 1)
@@ -462,8 +462,8 @@ def run_c3(args):
             },
             "roofline": {
                 "bound": "hbm",
-                "kernel": ("fused2_kernel<cdf97_nssplit_fwd, f32>: levels 0+1 in one kernel (16384^2 -> "
-                           "HL/LH/HH 8192^2 + 4 x 4096^2; two footprint-bounded launches of 2048 level-1 rows)"
+                "kernel": ("fused2_kernel<cdf97_nssplit_fwd, f32>: levels 0+1 in one launch (16384^2 -> "
+                           "HL/LH/HH 8192^2 + 4 x 4096^2; level 0's LL stays in shared memory)"
                            if g0b > g0a else
                            "stream_kernel<cdf97_nssplit_fwd, f32> level 0 (16384^2 -> 4 x 8192^2; two "
                            "footprint-bounded launches of 4096 quad rows)"),
@@ -472,7 +472,7 @@ def run_c3(args):
                 "peak_source": peak_src,
                 "unit": "GB/s",
                 "frac": achieved / peak,
-                "traffic": _traffic(f"c3_level0_{args.arith}"),
+                "traffic": _traffic(f"c3_group0_{args.arith}" if g0b > g0a else f"c3_level0_{args.arith}"),
                 "alg_bytes_per_launch": l0_bytes,
                 "alg_bytes_rule": "SURVEY 8(d): 8 B/px of every level the launch processes",
                 "compulsory_bytes": l0_compulsory,

@@ -610,8 +610,15 @@ int64_t fuse2_min_quads() {
 }
 
 // Levels at which b2dwt_dwt may start a fused pair (greedy from level 0 by
-// default); B2DWT_FUSE2_PAIRS="0,3" e.g. pairs (0,1) and (3,4) only.
-bool fuse2_starts_at(int level) {
+// default); B2DWT_FUSE2_PAIRS="0,3" e.g. pairs (0,1) and (3,4) only.  Strict
+// plans pair only with B2DWT_FUSE2_STRICT=1: their separately rounded products
+// make the fused kernel issue-bound (measured C3: 0.614 ms fused vs 0.569 ms
+// unfused), while fast plans gain (0.512 vs 0.548 ms).
+bool fuse2_starts_at(const b2dwt_plan_s& p, int level) {
+  if (strict_of(&p)) {
+    const char* s = std::getenv("B2DWT_FUSE2_STRICT");
+    if (!s || std::atoi(s) == 0) return false;
+  }
   const char* e = std::getenv("B2DWT_FUSE2_PAIRS");
   if (!e) return true;
   for (const char* p = e; *p;) {
@@ -674,10 +681,15 @@ int run_fused2_pair(const b2dwt_plan_s& p, const void* in, int64_t in_ld, int64_
   r.min_rows1 = std::max(8, min_rows() / 2);
   r.pdl = split_param(4) != 0;
   r.stream = stream;
-  // footprint-bounded launches, as run_fused: row bands of <= max_launch_bytes of input
+  // footprint-bounded launches, as run_fused: row bands of <= 1 GiB of input
+  // (B2DWT_F2_MAX_LAUNCH_BYTES): measured on C3 (1 GiB in), one launch runs
+  // levels 0+1 in 437 us against 460 us as two 512 MiB bands -- each band
+  // pays a ramp and a tail, and the translation-reach penalty that makes the
+  // stream kernel split (65536^2) only sets in beyond that
   const int64_t rows1 = rows / 2;
   const int64_t in_bytes = rows * cols * 16;
-  const int64_t cap = max_launch_bytes();
+  const char* cap_env = std::getenv("B2DWT_F2_MAX_LAUNCH_BYTES");
+  const int64_t cap = cap_env ? std::atoll(cap_env) : int64_t{1} << 30;
   int64_t parts = cap > 0 ? (in_bytes + cap - 1) / cap : 1;
   parts = std::max<int64_t>(1, std::min<int64_t>(parts, rows1 / 128));
   cudaError_t e = cudaSuccess;
@@ -1071,7 +1083,7 @@ int b2dwt_dwt(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t heig
   auto ll_half = [&](int level) { return in_sc == 0 ? 1 : in_sc == 1 ? 0 : (level == 0 ? 0 : 1); };
   for (int l = 0; l < levels; ++l) {
     const int64_t h = height >> l, w = width >> l;
-    if (l + 1 < levels && fuse2_starts_at(l)) {
+    if (l + 1 < levels && fuse2_starts_at(*plan, l)) {
       // levels l and l+1 in one kernel when the plan and geometry allow it
       const int half = ll_half(l + 1);
       void* ll1 = l + 1 == levels - 1 ? ll_out : sc[half];

@@ -51,7 +51,7 @@ constexpr int kF2SuperW = 224;  // level-l quads per CTA super-strip
 constexpr int kF2StripW = 60;   // level-l quads between the warps' strips
 constexpr int kF2Lead = 8;      // level-l quads loaded left of the CTA's columns
 #ifndef B2DWT_F2_RING
-#define B2DWT_F2_RING 6
+#define B2DWT_F2_RING 5  // 6 slots push a CTA past a third of the SM's shared memory (2 CTAs/SM)
 #endif
 constexpr int kF2Ring = B2DWT_F2_RING;  // ring slots (level-(l+1) rows)
 constexpr int kF2J = 116;               // ring columns (level-(l+1) quads)
