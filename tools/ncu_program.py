@@ -1,19 +1,14 @@
-"""ncu target: one forward or inverse of one built-in program on an N x N f32 image.
-    python tools/ncu_program.py <wavelet> <scheme> <fwd|inv> [N]"""
+"""One 8192^2 forward of one program (ncu target): SCHEME, WAVELET, FAST env."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1705_08266_b200 import CDF53, CDF97, Transform, build_scheme
-
-wavelet, scheme, direction = sys.argv[1:4]
-n = int(sys.argv[4]) if len(sys.argv) > 4 else 8192
-tr = Transform(build_scheme(scheme, {"cdf53": CDF53, "cdf97": CDF97}[wavelet]), "single", fast=True)
-x = torch.rand((n, n), device="cuda")
+plan = CDF97 if os.environ.get("WAVELET", "cdf97") == "cdf97" else CDF53
+tr = Transform(build_scheme(os.environ.get("SCHEME", "separable-convolution"), plan), "single",
+               fast=os.environ.get("FAST", "1") == "1", tile=False)
+x = torch.rand((8192, 8192), device="cuda")
 q = tr.forward(x)
-torch.cuda.synchronize()
-if direction == "fwd":
+for _ in range(3):
     tr.forward(x, out=q)
-else:
-    tr.inverse(*q, out=x)
 torch.cuda.synchronize()
-print("ok", tr.fwd_plan.key if direction == "fwd" else tr.inv_plan.key)
+print("ok", tr.fwd_plan.key)
