@@ -73,15 +73,30 @@ struct Arith<false> {
   static __device__ __forceinline__ double mac(double acc, double x, double k) { return fma(x, k, acc); }
 };
 
-// Fast mode's one contraction, made explicit: when a target's first term is a
-// product and its second a unit term, the pair is evaluated as one fused
-// multiply-add, fma(x0, k0, x1) (what a contracting compiler would emit for
-// x0 * k0 + x1, but fixed here so every kernel computes the same bits).
-// defer(K, count, unit_K, unit_next): term K's product is deferred to K + 1.
-template <bool kStrict>
-struct FastJoin {
-  B2DWT_HD static constexpr bool defer(int k, int count, bool unit_k, bool unit_next) {
-    return !kStrict && k == 0 && count > 1 && !unit_k && unit_next;
+// Evaluation order of a target's terms.  Strict: the compiled order
+// (engine.py:267), separately rounded.  Fast: the target's unit term first
+// (when it has exactly one: acc = x), then every product in compiled order as
+// one fused multiply-add -- the contraction a compiler might apply to
+// x0 * k0 + x1 made explicit and applied to every target, so each product is
+// exactly one FMA and every fast kernel (stream, two-level fused, tile)
+// computes the same bits.  at(base, count, k) = offset of the k-th evaluated term.
+template <class P, bool kStrict>
+struct TermOrder {
+  B2DWT_HD static constexpr int unit_pos(int base, int count) {
+    int u = -1, n = 0;
+    for (int k = 0; k < count; ++k)
+      if (P::term(base + k).unit) {
+        u = k;
+        ++n;
+      }
+    return n == 1 ? u : -1;
+  }
+  B2DWT_HD static constexpr int at(int base, int count, int k) {
+    if (kStrict) return k;
+    const int u = unit_pos(base, count);
+    if (u < 0) return k;
+    if (k == 0) return u;
+    return k <= u ? k - 1 : k;
   }
 };
 

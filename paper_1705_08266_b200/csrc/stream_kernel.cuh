@@ -316,23 +316,16 @@ struct Stage<P, T, Q, kStrict, S, false> {
   template <int OFF, int TGT, int K, class Args>
   __device__ __forceinline__ static void term(const T (&win)[NW][4][E], T (&acc)[Q], const Args& a) {
     constexpr int base = P::begin(S * 4 + TGT);
-    constexpr int idx = base + K;
     constexpr int cnt = P::begin(S * 4 + TGT + 1) - base;
+    constexpr int idx = base + TermOrder<P, kStrict>::at(base, cnt, K);  // fast: unit term first
     constexpr TermInfo ti = P::term(idx);
     constexpr int slot = cmod(OFF + ti.dn, NW);
-    // fast mode: a leading product followed by a unit term is ONE fused
-    // multiply-add (FastJoin, common.cuh)
-    constexpr bool kDefer = FastJoin<kStrict>::defer(K, cnt, ti.unit, K + 1 < cnt && P::term(idx + 1).unit);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const T x = win[slot][ti.src][L + q + ti.dm];
       constexpr T kc = static_cast<T>(P::coef(idx));  // liftfuse: dtype.type(coeff), engine.py:357
       if constexpr (K == 0) {
-        if constexpr (!kDefer) acc[q] = ti.unit ? x : Ar::mul(x, kc);
-      } else if constexpr (K == 1 && FastJoin<kStrict>::defer(0, cnt, P::term(base).unit, ti.unit)) {
-        constexpr TermInfo t0 = P::term(base);
-        constexpr T k0 = static_cast<T>(P::coef(base));
-        acc[q] = Ar::mac(x, win[cmod(OFF + t0.dn, NW)][t0.src][L + q + t0.dm], k0);
+        acc[q] = ti.unit ? x : Ar::mul(x, kc);
       } else {
         acc[q] = ti.unit ? Ar::add(acc[q], x) : Ar::mac(acc[q], x, kc);
       }

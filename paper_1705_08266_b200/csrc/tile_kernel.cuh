@@ -143,10 +143,10 @@ struct TileStep {
   using State = T[TG::kPer][4];
 
   template <int S, int TGT, int KT>
-  __device__ __forceinline__ static void term(T& acc, T& pend, const State& v, const T* sm, int k) {
+  __device__ __forceinline__ static void term(T& acc, const State& v, const T* sm, int k) {
     constexpr int base = P::begin(S * 4 + TGT);
-    constexpr int idx = base + KT;
     constexpr int cnt = P::begin(S * 4 + TGT + 1) - base;
+    constexpr int idx = base + TermOrder<P, kStrict>::at(base, cnt, KT);  // fast: unit term first (common.cuh)
     constexpr TermInfo ti = P::term(idx);
     constexpr T kc = static_cast<T>(P::coef(idx));  // liftfuse: dtype.type(coeff), engine.py:357
     T x;
@@ -155,15 +155,8 @@ struct TileStep {
     } else {
       x = sm[TG::plane_of(TG::stencil_rank(S), ti.src) + ti.dn * WC + ti.dm + threadIdx.x + k * kTileThreads];
     }
-    // fast mode: a leading product followed by a unit term is one fused
-    // multiply-add (FastJoin, common.cuh), as in the stream kernel
     if constexpr (KT == 0) {
-      if constexpr (FastJoin<kStrict>::defer(0, cnt, ti.unit, cnt > 1 && P::term(idx + 1).unit))
-        pend = x;
-      else
-        acc = ti.unit ? x : Ar::mul(x, kc);
-    } else if constexpr (KT == 1 && FastJoin<kStrict>::defer(0, cnt, P::term(base).unit, ti.unit)) {
-      acc = Ar::mac(x, pend, static_cast<T>(P::coef(base)));
+      acc = ti.unit ? x : Ar::mul(x, kc);
     } else {
       acc = ti.unit ? Ar::add(acc, x) : Ar::mac(acc, x, kc);
     }
@@ -171,8 +164,8 @@ struct TileStep {
 
   template <int S, int TGT, int... KT>
   __device__ __forceinline__ static T target(const State& v, const T* sm, int k, std::integer_sequence<int, KT...>) {
-    T acc = T(0), pend = T(0);
-    (term<S, TGT, KT>(acc, pend, v, sm, k), ...);
+    T acc = T(0);
+    (term<S, TGT, KT>(acc, v, sm, k), ...);
     return acc;
   }
 

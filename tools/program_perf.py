@@ -29,9 +29,13 @@ def t(fn, reps=15, per_graph=10):
     return statistics.median(ts)
 
 
-for fast in (True, False):
+only = os.environ.get("PROGRAMS")  # e.g. "cdf97/separable-convolution,cdf97/non-separable-split"
+arith = os.environ.get("ARITH", "fast,strict").split(",")
+for fast in [a == "fast" for a in arith]:
     for wname, plan in (("cdf53", CDF53), ("cdf97", CDF97)):
         for sname in SCHEME_NAMES:
+            if only and f"{wname}/{sname}" not in only.split(","):
+                continue
             tr = Transform(build_scheme(sname, plan), "single", fast=fast)
             q = tr.forward(x)
             rec = torch.empty_like(x)
