@@ -38,8 +38,12 @@
  *   - Boundary handling is the reference's whole-sample symmetric extension
  *     applied to the state entering every sub-step (engine.py:55-92, 312-347).
  *   - Calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy default
- *     stream).  No global mutable state; plans are immutable and may be shared
- *     across threads.
+ *     stream).  Plans are immutable and may be shared across threads.  The
+ *     library's only process-wide state is internal and lock-protected: per-
+ *     device caches (function attributes, SM counts) and zero-initialised
+ *     work-split counters (a pool per stream -- launches ordered on a stream
+ *     reuse them -- and a never-reused arena for launches captured into CUDA
+ *     graphs, which may replay concurrently with anything).
  *   - Return 0 on success or a negative B2DWT_E* code; b2dwt_last_error()
  *     returns a thread-local message.  There is no CPU fallback: without a
  *     CUDA device every compute entry point fails with B2DWT_ECUDA.

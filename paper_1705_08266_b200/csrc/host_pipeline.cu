@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -115,7 +116,39 @@ int b2dwt_dwt_host(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t
   // least one, never thinner than the cone) so the small levels are not cut
   // into copies too small to run at PCIe speed
   const int64_t cone = std::max<int64_t>(1, std::max(info.halo_up, info.halo_down));
-  const int K = std::max(1, bands > 0 ? bands : 16);
+  const int K0 = std::max(1, bands > 0 ? bands : 16);
+  // Upload chunks: K0 equal chunks plus a ramp of `ramp` chunks at each end
+  // whose sizes halve towards the image edges (1/2, 1/4, ... of a middle
+  // chunk), so the pipeline fills (first upload, nothing to download yet) and
+  // drains (last download, nothing left to upload) in a fraction of a chunk's
+  // copy time.  B2DWT_PIPE_RAMP overrides (0 = equal chunks).
+  static const int ramp_env = [] {
+    const char* v = std::getenv("B2DWT_PIPE_RAMP");
+    return v ? std::atoi(v) : 0;  // measured: no gain on C3 (the pipeline sits at the PCIe floor)
+  }();
+  const int64_t R0 = height / 2;
+  int ramp = std::max(0, std::min(ramp_env, K0 / 4));
+  std::vector<int64_t> qb;  // chunk boundaries in quad rows of level 0
+  for (;; --ramp) {
+    std::vector<double> wts;
+    for (int r = ramp; r >= 1; --r) wts.push_back(std::ldexp(1.0, -r));
+    for (int c = 0; c < K0; ++c) wts.push_back(1.0);
+    for (int r = 1; r <= ramp; ++r) wts.push_back(std::ldexp(1.0, -r));
+    double tot = 0;
+    for (double x : wts) tot += x;
+    qb.assign(1, 0);
+    double acc = 0;
+    for (double x : wts) {
+      acc += x;
+      qb.push_back(std::min<int64_t>(R0, static_cast<int64_t>(std::llround(R0 * acc / tot))));
+    }
+    qb.back() = R0;
+    // every ramp chunk must still hold more rows than the cone (small images: no ramp)
+    bool ok = true;
+    for (size_t c = 1; c < qb.size() && ok; ++c) ok = qb[c] - qb[c - 1] > 2 * cone;
+    if (ok || ramp == 0) break;
+  }
+  const int K = static_cast<int>(qb.size()) - 1;
   std::vector<int> KL(levels);
   for (int l = 0; l < levels; ++l) {
     const int64_t R = height >> (l + 1);
@@ -141,7 +174,7 @@ int b2dwt_dwt_host(b2dwt_plan plan, const void* image, int64_t image_ld, int64_t
   std::vector<cudaEvent_t> ev_in(K);
   std::vector<int64_t> chunk_end(K);  // pixel rows uploaded after chunk c
   for (int c = 0; c < K; ++c) {
-    const int64_t p0 = 2 * (height / 2 * c / K), p1 = 2 * (height / 2 * (c + 1) / K);
+    const int64_t p0 = 2 * qb[c], p1 = 2 * qb[c + 1];
     chunk_end[c] = p1;
     if (p1 > p0) {
       e = cudaMemcpy2DAsync(dimg + static_cast<size_t>(p0 * width) * es, width * es,

@@ -26,6 +26,13 @@ from dataclasses import dataclass
 __all__ = ["shard_range", "RowStrips", "StripLayout"]
 
 
+def _in_place(t):
+    """A message buffer that is the tensor itself (no staging copy)."""
+    if not t.is_contiguous():
+        raise ValueError("halo slices must be contiguous rows of the strip buffer")
+    return t
+
+
 def shard_range(n_items: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous, balanced [lo, hi) share of ``n_items`` for ``rank``."""
     if world < 1 or not 0 <= rank < world:
@@ -99,12 +106,13 @@ class RowStrips:
         L = self.layout(level)
         own = buf[L.halo_top:L.halo_top + L.rows]
         ops = []
+        # whole-row slices of a row-contiguous buffer: sent and received in place
         if self.rank > 0:
-            ops.append(dist.P2POp(dist.irecv, buf[:L.halo_top], self.rank - 1, group))
-            ops.append(dist.P2POp(dist.isend, own[:2 * self.down].contiguous(), self.rank - 1, group))
+            ops.append(dist.P2POp(dist.irecv, _in_place(buf[:L.halo_top]), self.rank - 1, group))
+            ops.append(dist.P2POp(dist.isend, _in_place(own[:2 * self.down]), self.rank - 1, group))
         if self.rank < self.world - 1:
-            ops.append(dist.P2POp(dist.isend, own[L.rows - 2 * self.up:].contiguous(), self.rank + 1, group))
-            ops.append(dist.P2POp(dist.irecv, buf[L.halo_top + L.rows:], self.rank + 1, group))
+            ops.append(dist.P2POp(dist.isend, _in_place(own[L.rows - 2 * self.up:]), self.rank + 1, group))
+            ops.append(dist.P2POp(dist.irecv, _in_place(buf[L.halo_top + L.rows:]), self.rank + 1, group))
         return dist.batch_isend_irecv(ops) if ops else []
 
     # -- compute ------------------------------------------------------------------
@@ -154,22 +162,26 @@ class RowStrips:
     # The inverse strips the four subband planes instead: rank r owns quad rows
     # [row0/2, (row0+rows)/2) of every plane plus `up` / `down` halo quad rows of
     # the INVERSE program's cone (construct the RowStrips with
-    # Transform.inv_plan.cone[:2]), exchanged per plane; bands go through
-    # ``band_inverse`` = Transform.inverse_rows, which reflects only at global
-    # edges, so the image rows are bit-identical to the single-GPU inverse.
+    # Transform.inv_plan.cone[:2]); bands go through ``band_inverse`` =
+    # Transform.inverse_rows, which reflects only at global edges, so the image
+    # rows are bit-identical to the single-GPU inverse.  The buffer is laid out
+    # [quad row, plane, column] so one quad row of all four planes is contiguous:
+    # each neighbour's halo travels as ONE packed message (not one per plane),
+    # and the kernel reads each plane with a row pitch of 4 x W/2.
 
     def _sub_halos(self):
         return (self.up if self.rank > 0 else 0), (self.down if self.rank < self.world - 1 else 0)
 
     def allocate_subbands(self, new_empty, level: int = 0):
-        """[4, halo_top + owned + halo_bot quad rows, W/2] buffer of the planes."""
+        """[halo_top + owned + halo_bot quad rows, 4, W/2] buffer of the planes."""
         L = self.layout(level)
         ht, hb = self._sub_halos()
-        return new_empty((4, ht + L.rows // 2 + hb, L.width // 2))
+        return new_empty((ht + L.rows // 2 + hb, 4, L.width // 2))
 
     def owned_subbands(self, sb, level: int = 0):
+        """The owned quad rows as a [4, rows, W/2] view (plane-major, pitched)."""
         ht, _ = self._sub_halos()
-        return sb[:, ht:ht + self.layout(level).rows // 2]
+        return sb[ht:ht + self.layout(level).rows // 2].permute(1, 0, 2)
 
     def exchange_subbands(self, sb, level: int = 0, group=None):
         """Post the per-plane halo send/recv of a subband buffer; returns the requests."""
@@ -177,15 +189,14 @@ class RowStrips:
 
         q = self.layout(level).rows // 2
         ht, hb = self._sub_halos()
-        ops = []
-        for c in range(4):
-            own = sb[c, ht:ht + q]
-            if self.rank > 0:
-                ops.append(dist.P2POp(dist.irecv, sb[c, :ht], self.rank - 1, group))
-                ops.append(dist.P2POp(dist.isend, own[:self.down].contiguous(), self.rank - 1, group))
-            if self.rank < self.world - 1:
-                ops.append(dist.P2POp(dist.isend, own[q - self.up:].contiguous(), self.rank + 1, group))
-                ops.append(dist.P2POp(dist.irecv, sb[c, ht + q:], self.rank + 1, group))
+        own = sb[ht:ht + q]
+        ops = []  # one packed message per neighbour and direction (all four planes' rows)
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.irecv, _in_place(sb[:ht]), self.rank - 1, group))
+            ops.append(dist.P2POp(dist.isend, _in_place(own[:self.down]), self.rank - 1, group))
+        if self.rank < self.world - 1:
+            ops.append(dist.P2POp(dist.isend, _in_place(own[q - self.up:]), self.rank + 1, group))
+            ops.append(dist.P2POp(dist.irecv, _in_place(sb[ht + q:]), self.rank + 1, group))
         return dist.batch_isend_irecv(ops) if ops else []
 
     def _run_inverse_band(self, band_inverse, sb, level, out_rows, out):
@@ -197,7 +208,7 @@ class RowStrips:
         buf_q0 = q0 - self._sub_halos()[0]  # global quad row of buffer row 0
         b0 = max(0, r0 - self.up)
         b1 = min(L.height // 2, r1 + self.down)
-        band = tuple(sb[c, b0 - buf_q0:b1 - buf_q0] for c in range(4))
+        band = tuple(sb[b0 - buf_q0:b1 - buf_q0, c] for c in range(4))  # pitched planes
         band_inverse(band, b0, L.height, r0, r1, out[2 * (r0 - q0):2 * (r1 - q0)])
 
     def inverse(self, band_inverse, sb, out, level: int = 0, group=None, overlap: bool = True):
