@@ -671,7 +671,7 @@ int run_fused2_pair(const b2dwt_plan_s& p, const void* in, int64_t in_ld, int64_
     const char* e = std::getenv("B2DWT_F2_TAIL_ROWS");
     return e ? std::atoi(e) : 16;
   }();
-  static const int f2_edge = [] {
+  static const int f2_edge = [] {  // 8 (kF2Edge): sized per launch for small ones (f2_work_space)
     const char* e = std::getenv("B2DWT_F2_EDGE_ROWS");
     return e ? std::atoi(e) : 8;
   }();

@@ -89,6 +89,7 @@ struct Fused2Args {
   // unit); with a tail counter the edge units are the first dynamic items
   // (dyn_edges) and the interior past static_end follows in tail chunks.
   int top, bot, ki0, rows_in, n_edge, unit_cost, edge_cost;
+  int unit_rows, units_top, units_bot;  // an edge band is cut into units of unit_rows rows
   int total, static_begin, static_end, dyn_edges, n_dyn;
 };
 
@@ -100,14 +101,28 @@ struct Fused2Args {
 template <class T>
 inline void f2_work_space(Fused2Args<T>& a, int static_frac, int edge_rows = kF2Edge) {
   const int rows1 = a.rows / 2;
-  const int edge = edge_rows < 1 ? 1 : edge_rows;
+  int edge = edge_rows < 1 ? 1 : edge_rows;
+  if (a.tail_counter == nullptr && edge_rows == kF2Edge) {
+    // small launch, all static: its time is max(edge unit, CTA share), an edge
+    // unit costing ~4 interior rows per row -- size it to one share (>= 3 rows,
+    // the fewest that leave the interior units unchecked).  C3 levels 2+3
+    // (share 23 rows): 6-row units 45 us, 8-row 49 us.
+    const int share = static_cast<int>(int64_t{a.n_super} * (a.k_end - a.k_begin) / (a.n_ctas > 0 ? a.n_ctas : 1));
+    edge = (share + 2) / 4;
+    edge = edge < 3 ? 3 : edge > kF2Edge ? kF2Edge : edge;
+  }
   a.top = a.k_begin == 0 ? (a.k_end - a.k_begin < edge ? a.k_end - a.k_begin : edge) : 0;
   const int rest = a.k_end - a.k_begin - a.top;
   a.bot = a.k_end == rows1 ? (rest < edge ? rest : edge) : 0;
   a.ki0 = a.k_begin + a.top;
   a.rows_in = a.k_end - a.bot - a.ki0;
-  a.n_edge = (a.top > 0 ? a.n_super : 0) + (a.bot > 0 ? a.n_super : 0);
-  a.unit_cost = 6 * edge;  // checked ticks at both levels plus both cones, per edge unit
+  // one unit per edge band (cutting it finer multiplies the checked cones:
+  // 2-row units took C3 levels 2+3 from 47 to 57 us)
+  a.unit_rows = edge;
+  a.units_top = (a.top + a.unit_rows - 1) / a.unit_rows;
+  a.units_bot = (a.bot + a.unit_rows - 1) / a.unit_rows;
+  a.n_edge = a.n_super * (a.units_top + a.units_bot);
+  a.unit_cost = 4 * a.unit_rows;  // checked ticks at both levels plus both cones (measured ~4x an interior row)
   a.edge_cost = a.n_edge * a.unit_cost;
   a.total = a.edge_cost + a.n_super * a.rows_in;
   if (a.tail_counter != nullptr) {
@@ -379,10 +394,17 @@ __global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
           continue;
         }
         f = (e + 1) * a.unit_cost;
-        const bool is_top = a.top > 0 && e < a.n_super;
-        sup = is_top ? e : e - (a.top > 0 ? a.n_super : 0);
-        k0 = is_top ? a.k_begin : a.k_end - a.bot;
-        k1 = is_top ? a.k_begin + a.top : a.k_end;
+        const int n_top = a.n_super * a.units_top;
+        if (e < n_top) {  // top band: super-strip e / units_top, its sub-unit e % units_top
+          sup = e / a.units_top;
+          k0 = a.k_begin + (e - sup * a.units_top) * a.unit_rows;
+          k1 = min(a.k_begin + a.top, k0 + a.unit_rows);
+        } else {
+          const int eb = e - n_top;
+          sup = eb / a.units_bot;
+          k0 = a.k_end - a.bot + (eb - sup * a.units_bot) * a.unit_rows;
+          k1 = min(a.k_end, k0 + a.unit_rows);
+        }
       } else {  // interior rows
         const int g = f - a.edge_cost;
         sup = g / a.rows_in;
