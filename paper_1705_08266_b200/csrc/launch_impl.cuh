@@ -45,6 +45,23 @@ struct Shape<double> {
   static constexpr int kWarps = 4, kStages = 3, kRps = 2;
 };
 
+// Per program: f32 programs whose tick period does not divide the ring's 4 rows
+// per stage (the separable convolutions: vertical windows of 3 or 5 rows) get
+// stages of `period` rows at the same ring bytes per warp, so the steady loop
+// switches stages once per period instead of testing every row (CDF 9/7
+// convolution: ~55 of 1153 loop instructions per 5 rows were that test and
+// the TMA issue path).
+template <class P, class T>
+struct ShapeFor : Shape<T> {};
+template <class P>
+struct ShapeFor<P, float> : Shape<float> {
+  static constexpr int kPer = Geo<P>::kPeriod;
+  static constexpr bool kOdd = (Shape<float>::kRps % kPer) != 0 && kPer <= 8;
+  static constexpr int kRps = kOdd ? kPer : Shape<float>::kRps;
+  static constexpr int kStages =
+      kOdd ? (Shape<float>::kStages * Shape<float>::kRps) / kPer : Shape<float>::kStages;
+};
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -108,7 +125,7 @@ int num_sms() {
 
 template <class Prog, class T, int LIN, int LOUT, bool kStrict, bool kTma>
 cudaError_t launch(const FusedLaunch& r) {
-  using S = Shape<T>;
+  using S = ShapeFor<Prog, T>;
   using Args = StreamArgs<T, (Prog::kNumTerms > 0 ? Prog::kNumTerms : 1)>;
   constexpr int kWarps = S::kWarps, kStages = S::kStages, kRps = S::kRps, kQ = S::kQ;
   auto kern = stream_kernel<Prog, T, kQ, LIN, LOUT, kStrict, kTma, kWarps, kStages, kRps>;
