@@ -610,14 +610,13 @@ int64_t fuse2_min_quads() {
 }
 
 // Levels at which b2dwt_dwt may start a fused pair (greedy from level 0 by
-// default); B2DWT_FUSE2_PAIRS="0,3" e.g. pairs (0,1) and (3,4) only.  Strict
-// plans pair only with B2DWT_FUSE2_STRICT=1: their separately rounded products
-// make the fused kernel issue-bound (measured C3: 0.614 ms fused vs 0.569 ms
-// unfused), while fast plans gain (0.512 vs 0.548 ms).
+// default); B2DWT_FUSE2_PAIRS="0,3" e.g. pairs (0,1) and (3,4) only.
+// B2DWT_FUSE2_STRICT=0 keeps strict plans at one launch per level (measured
+// C3 strict: 0.5105 ms fused vs 0.567 ms unfused; fast 0.476 vs 0.546 ms).
 bool fuse2_starts_at(const b2dwt_plan_s& p, int level) {
   if (strict_of(&p)) {
     const char* s = std::getenv("B2DWT_FUSE2_STRICT");
-    if (!s || std::atoi(s) == 0) return false;
+    if (s && std::atoi(s) == 0) return false;
   }
   const char* e = std::getenv("B2DWT_FUSE2_PAIRS");
   if (!e) return true;

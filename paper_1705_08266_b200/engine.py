@@ -849,8 +849,8 @@ class PyramidGraph:
         import os
 
         min_quads = int(os.environ.get("B2DWT_FUSE2_MIN_QUADS", 1 << 20))
-        if not (tr.flags & _native.FAST) and os.environ.get("B2DWT_FUSE2_STRICT", "0") in ("", "0"):
-            min_quads = 0  # strict plans run one launch per level (b2dwt_host.cu fuse2_starts_at)
+        if not (tr.flags & _native.FAST) and os.environ.get("B2DWT_FUSE2_STRICT", "1") == "0":
+            min_quads = 0  # strict plans held at one launch per level (b2dwt_host.cu fuse2_starts_at)
         starts = os.environ.get("B2DWT_FUSE2_PAIRS")
         starts = None if starts is None else {int(v) for v in starts.split(",") if v.strip()}
         h, w = self.x.shape

@@ -47,7 +47,7 @@ def test_forward2_equals_two_launches(shape, fast):
 @pytest.mark.parametrize("wavelet,scheme", FUSABLE, ids=[f"{w}-{s}" for w, s in FUSABLE])
 def test_fused_pyramid_equals_unfused_and_oracle(wavelet, scheme, monkeypatch):
     monkeypatch.setenv("B2DWT_FUSE2_MIN_QUADS", "1")  # fuse every pair b2dwt_dwt can
-    monkeypatch.setenv("B2DWT_FUSE2_STRICT", "1")  # strict plans too (off by default: slower there)
+
     s = build_scheme(scheme, PLANS[wavelet])
     h, w = 1032, 1544  # ragged super-strips at both fused pairs; 3 levels: pair + single
     img = np.random.default_rng(9).random((h, w)).astype(np.float32)
@@ -94,7 +94,6 @@ def test_two_fused_pairs_in_one_pyramid(fast, monkeypatch):
     scratch half and must write its LL into the other (b2dwt_dwt), also inside
     the captured graph and its per-group event variant."""
     monkeypatch.setenv("B2DWT_FUSE2_MIN_QUADS", "1")
-    monkeypatch.setenv("B2DWT_FUSE2_STRICT", "1")
     s = build_scheme("non-separable-split", CDF97)
     img = np.random.default_rng(2).random((1024, 1536)).astype(np.float32)
     x = torch.from_numpy(img).cuda()
@@ -120,12 +119,14 @@ def test_two_fused_pairs_in_one_pyramid(fast, monkeypatch):
         assert np.array_equal(a_ll.cpu().numpy(), want_ll)
 
 
-def test_fusion_policy_fast_only_by_default():
+def test_fusion_policy(monkeypatch):
     x = torch.rand((2048, 2048), device="cuda")
     s = build_scheme("non-separable-split", CDF97)
     assert Transform(s, "single", fast=True).capture_dwt(x, 3).groups == [(0, 1), (2, 2)]
-    assert Transform(s, "single").capture_dwt(x, 3).groups == [(0, 0), (1, 1), (2, 2)]
+    assert Transform(s, "single").capture_dwt(x, 3).groups == [(0, 1), (2, 2)]
     assert Transform(s, "single", fast=True, fuse=False).capture_dwt(x, 3).groups == [(0, 0), (1, 1), (2, 2)]
+    monkeypatch.setenv("B2DWT_FUSE2_STRICT", "0")
+    assert Transform(s, "single").capture_dwt(x, 3).groups == [(0, 0), (1, 1), (2, 2)]
 
 
 def test_unfusable_requests_fall_back():
