@@ -176,8 +176,15 @@ cudaError_t launch(const FusedLaunch& r) {
   using C = Cone<Prog>;
   constexpr int kInQuadBytes = static_cast<int>(sizeof(T)) * (LIN == kLayoutInterleaved ? 2 : 1);
   constexpr int kOutQuadBytes = static_cast<int>(sizeof(T)) * (LOUT == kLayoutInterleaved ? 2 : 1);
-  const int halo_align = std::max({2, std::min(4, 32 / kInQuadBytes), 16 / kInQuadBytes, r.strip_align});
-  const int width_align = std::max(halo_align, 32 / kOutQuadBytes);
+  // B2DWT_STRIP_PACK=1 (experiment): strips packed at the cone (16-B box
+  // starts, strip widths not sector multiples)
+  static const bool pack = [] {
+    const char* e = std::getenv("B2DWT_STRIP_PACK");
+    return e && std::atoi(e) != 0;
+  }();
+  const int halo_align = pack ? std::max(2, 16 / kInQuadBytes)
+                              : std::max({2, std::min(4, 32 / kInQuadBytes), 16 / kInQuadBytes, r.strip_align});
+  const int width_align = pack ? halo_align : std::max(halo_align, 32 / kOutQuadBytes);
   const int halo_l = (C::left + halo_align - 1) / halo_align * halo_align;
   int strip_w = kLaneCount * kQ - halo_l - C::right;
   strip_w = strip_w / width_align * width_align;

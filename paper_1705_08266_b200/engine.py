@@ -909,6 +909,7 @@ def _call_workspace(torch, nbytes, stream):
 
 _TRANSFORMS: "OrderedDict" = None
 _TRANSFORMS_MAX = 16
+_SCHEME_KEYS: dict = {}  # id(scheme) -> (weakref to it, compiled-program key)
 
 
 def _transform(scheme, precision: str) -> Transform:
@@ -916,12 +917,25 @@ def _transform(scheme, precision: str) -> Transform:
     (not the scheme object's identity: callers that rebuild the scheme per call
     reuse one entry) in a small LRU; entries hold no device workspace."""
     global _TRANSFORMS
+    import weakref
     from collections import OrderedDict
 
     if _TRANSFORMS is None:
         _TRANSFORMS = OrderedDict()
-    fwd, inv = _programs(scheme)
-    key = (_signature(fwd), _signature(inv), precision)
+    # fast path: the same scheme object again (compiling + inverting a scheme
+    # costs ~1 ms, as much as a whole 1024^2 host-array call) -- held weakly
+    hit = _SCHEME_KEYS.get(id(scheme))
+    key = hit[1] if hit is not None and hit[0]() is scheme else None
+    if key is None:
+        fwd, inv = _programs(scheme)
+        key = (_signature(fwd), _signature(inv))
+        try:
+            _SCHEME_KEYS[id(scheme)] = (weakref.ref(scheme), key)
+            while len(_SCHEME_KEYS) > 4 * _TRANSFORMS_MAX:
+                _SCHEME_KEYS.pop(next(iter(_SCHEME_KEYS)))
+        except TypeError:  # not weakly referenceable: no fast path
+            pass
+    key = key + (precision,)
     t = _TRANSFORMS.get(key)
     if t is None:
         t = Transform(scheme, precision)
@@ -947,11 +961,11 @@ def _to_host(t) -> np.ndarray:
 def forward(image: Image2D, scheme, cfg: TileConfig | None = None) -> SubbandQuad:
     """Single-level forward transform of an even-dimensioned image (engine.py:481-487)."""
     cfg = cfg or TileConfig()
-    program = compile_scheme(scheme)
     a = image.data
     if a.shape[0] % 2 or a.shape[1] % 2:
         raise ValueError(f"dimensions must be even, got {a.shape[1]}x{a.shape[0]}")
-    _check_tile(cfg, program)
+    if cfg.tile is not None:  # (compiling costs ~0.3 ms: only when there is a tile to check)
+        _check_tile(cfg, compile_scheme(scheme))
     torch = _require_cuda()
     tr = _transform(scheme, image.precision)
     h, w = a.shape
@@ -965,8 +979,8 @@ def forward(image: Image2D, scheme, cfg: TileConfig | None = None) -> SubbandQua
 def inverse(quad: SubbandQuad, scheme, cfg: TileConfig | None = None) -> Image2D:
     """Invert :func:`forward`; ``scheme`` is the forward scheme (engine.py:490-495)."""
     cfg = cfg or TileConfig()
-    program = compile_scheme(invert_scheme(_adopt_scheme(scheme)))
-    _check_tile(cfg, program)
+    if cfg.tile is not None:
+        _check_tile(cfg, compile_scheme(invert_scheme(_adopt_scheme(scheme))))
     torch = _require_cuda()
     tr = _transform(scheme, quad.ll.precision)
     comps = [_to_device(torch, c) for c in quad.components()]
@@ -1046,7 +1060,8 @@ def run_reference(program, comps) -> list:
 def dwt(image: Image2D, scheme, levels: int = 1, cfg: TileConfig | None = None) -> Pyramid:
     """Multi-level forward transform: level l is :func:`forward` of level l-1's LL."""
     cfg = cfg or TileConfig()
-    _check_tile(cfg, compile_scheme(scheme))
+    if cfg.tile is not None:
+        _check_tile(cfg, compile_scheme(scheme))
     torch = _require_cuda()
     tr = _transform(scheme, image.precision)
     a = image.data
