@@ -170,3 +170,24 @@ def test_graph_replay_concurrent_with_other_stream_launches():
     for a, b in zip(g.details, want_det):
         for u, v in zip(a, b):
             assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_shapes_fused_pair_equals_two_launches(seed):
+    """Random geometry: heights from the edge-units-only regime to many static
+    units, widths across partial super-strips, padded pitches, both modes."""
+    rng = np.random.default_rng(100 + seed)
+    for trial in range(8):
+        h = 4 * int(rng.integers(4, 400))
+        w = 4 * int(rng.integers(64, 800))
+        pad = 4 * int(rng.integers(0, 9))
+        fast = bool(rng.integers(0, 2))
+        wavelet, scheme = FUSABLE[int(rng.integers(0, len(FUSABLE)))]
+        tr = Transform(build_scheme(scheme, PLANS[wavelet]), "single", fast=fast)
+        base = torch.rand((h, w + pad), device="cuda", generator=torch.Generator(device="cuda").manual_seed(trial))
+        x = base[:, :w]
+        got = tr.forward2(x)
+        assert got is not None, (h, w)
+        want = _two_launches(tr, x.contiguous())
+        for g, wv in zip(got[0] + got[1], want[0] + want[1]):
+            assert torch.equal(g, wv), (seed, trial, h, w, pad, fast, wavelet, scheme)
