@@ -81,7 +81,7 @@ struct Fused2Args {
   unsigned long long* tail_counter;  // [0] tickets, [1] CTAs done (self-resetting), or null
   int tail_chunk;                    // level-(l+1) rows per dynamic chunk
   // work space (f2_work_space on the host), in cost units of one interior
-  // level-(l+1) row: [0, edge_cost) = the n_edge checked units of kF2Edge rows
+  // level-(l+1) row: [0, edge_cost) = the n_edge checked units of unit_rows rows
   // at the image top / bottom (`top` / `bot` rows per super-strip), each
   // costing unit_cost; then [edge_cost, total) = interior rows [ki0, ki0 +
   // rows_in) of every super-strip.  [static_begin, static_end) is split evenly
@@ -93,11 +93,12 @@ struct Fused2Args {
   int total, static_begin, static_end, dyn_edges, n_dyn;
 };
 
-// Host: fill the work-space fields of `a` (its k range, n_super, tail_counter,
-// tail_chunk and rows already set).  The rows within kF2Edge of the image top /
-// bottom need the checked (reflecting) path at both levels and run as short
-// separate units, so no long segment is ever checked; they sit at the head of
-// the static split, weighted by their cost (checked ticks plus both cones).
+// Host: fill the work-space fields of `a` (its k range, n_super, n_ctas,
+// tail_counter, tail_chunk and rows already set).  The rows near the image top
+// / bottom need the checked (reflecting) path at both levels and run as short
+// separate units, so no long segment is ever checked.  Large launches (with a
+// tail counter) hand them out first in the dynamic queue; small ones weight
+// them into the static split and size them to one CTA's share.
 template <class T>
 inline void f2_work_space(Fused2Args<T>& a, int static_frac, int edge_rows = kF2Edge) {
   const int rows1 = a.rows / 2;
