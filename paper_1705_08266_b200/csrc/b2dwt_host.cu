@@ -129,7 +129,7 @@ namespace {
 
 bool strict_of(const b2dwt_plan_s* p) { return (p->flags & B2DWT_FAST) == 0; }
 
-// Zero-initialised {tickets, done} counter pairs for the dynamic work tail.
+// Zero-initialised counter slots (kSlotWords words) for the dynamic work tail.
 // The kernel's last CTA resets its pair, so launches ordered on ONE stream can
 // share pairs safely; launches that may run concurrently must not.  Hence:
 //   * eager launches draw round-robin from a pool owned by their stream;
@@ -141,6 +141,7 @@ bool strict_of(const b2dwt_plan_s* p) { return (p->flags & B2DWT_FAST) == 0; }
 namespace {
 constexpr int kStreamSlots = 64;
 constexpr int kArenaSlots = 4096;
+constexpr int kSlotWords = 4;  // [0] claimed tail units, [1] CTAs done, [2] edge tickets, [3] spare
 struct DeviceCounters {
   std::unordered_map<cudaStream_t, std::pair<unsigned long long*, unsigned>> streams;
   unsigned long long* arena = nullptr;
@@ -148,12 +149,12 @@ struct DeviceCounters {
 };
 unsigned long long* zeroed_pairs(int n) {
   void* p = nullptr;
-  if (cudaMalloc(&p, static_cast<size_t>(n) * 2 * sizeof(unsigned long long)) != cudaSuccess) {
+  if (cudaMalloc(&p, static_cast<size_t>(n) * kSlotWords * sizeof(unsigned long long)) != cudaSuccess) {
     (void)cudaGetLastError();
     return nullptr;
   }
   // synchronous zeroing, complete before any stream can use the pairs
-  if (cudaMemset(p, 0, static_cast<size_t>(n) * 2 * sizeof(unsigned long long)) != cudaSuccess ||
+  if (cudaMemset(p, 0, static_cast<size_t>(n) * kSlotWords * sizeof(unsigned long long)) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess) {
     (void)cudaGetLastError();
     cudaFree(p);
@@ -178,7 +179,7 @@ unsigned long long* tail_counter_slot(cudaStream_t stream) {
   DeviceCounters& d = dev_counters[dev];
   if (cap != cudaStreamCaptureStatusNone) {
     if (!d.arena || d.arena_used >= kArenaSlots) return nullptr;  // no allocation inside a capture
-    return d.arena + 2 * (d.arena_used++);
+    return d.arena + kSlotWords * (d.arena_used++);
   }
   if (!d.arena || d.arena_used >= kArenaSlots) {  // (re)fill the capture arena while we may allocate
     d.arena = zeroed_pairs(kArenaSlots);
@@ -190,7 +191,23 @@ unsigned long long* tail_counter_slot(cudaStream_t stream) {
     if (!p) return nullptr;
     it = d.streams.emplace(stream, std::make_pair(p, 0u)).first;
   }
-  return it->second.first + 2 * (it->second.second++ % kStreamSlots);
+  return it->second.first + kSlotWords * (it->second.second++ % kStreamSlots);
+}
+
+// Guided self-scheduling of the dynamic tail (claim_guided, stream_kernel.cuh).
+// Measured: the two-level fused kernel gains (C3 levels 0+1 427 -> 408 us with a
+// 768/1024 static share), the stream kernel does not (C4 +1.6%, C5 -1%), so the
+// defaults differ.  B2DWT_GUIDED / B2DWT_F2_GUIDED override (0 / 1).
+int guided_tail(bool fused2) {
+  static const int v[2] = {[] {
+                             const char* e = std::getenv("B2DWT_GUIDED");
+                             return e ? std::atoi(e) : 0;
+                           }(),
+                           [] {
+                             const char* e = std::getenv("B2DWT_F2_GUIDED");
+                             return e ? std::atoi(e) : 1;
+                           }()};
+  return v[fused2 ? 1 : 0];
 }
 
 // Lower bound on rows per CTA (B2DWT_MIN_ROWS overrides).
@@ -535,6 +552,7 @@ int run_fused(const b2dwt_plan_s& p, FusedLaunch& r) {
   r.tail_counter = split_param(0) < 1024 ? tail_counter_slot(r.stream) : nullptr;
   r.static_frac = split_param(0);
   r.tail_rows = split_param(1);
+  r.guided = guided_tail(false);
   r.strip_align = split_param(2);
   r.full_rows = split_param(3);
   r.pdl = split_param(4) != 0;
@@ -662,9 +680,9 @@ int run_fused2_pair(const b2dwt_plan_s& p, const void* in, int64_t in_ld, int64_
   // work split of the fused kernel: a unit re-reads the cones of BOTH levels
   // (~14 level-l rows), so its dynamic tail chunks are longer than the stream
   // kernel's.  B2DWT_F2_STATIC_FRAC / B2DWT_F2_TAIL_ROWS override.
-  static const int f2_static = [] {  // measured on C3 (tools/f2_sweep.sh): 896-928 best
+  static const int f2_static = [] {  // measured on C3 (tools/tail_sweep.sh): 768 with guided claims
     const char* e = std::getenv("B2DWT_F2_STATIC_FRAC");
-    return e ? std::atoi(e) : 912;
+    return e ? std::atoi(e) : 768;
   }();
   static const int f2_tail = [] {
     const char* e = std::getenv("B2DWT_F2_TAIL_ROWS");
@@ -676,6 +694,7 @@ int run_fused2_pair(const b2dwt_plan_s& p, const void* in, int64_t in_ld, int64_
   }();
   r.static_frac = f2_static;
   r.tail_rows1 = f2_tail;
+  r.guided = guided_tail(true);
   r.edge_rows1 = f2_edge;
   r.min_rows1 = std::max(8, min_rows() / 2);
   r.pdl = split_param(4) != 0;

@@ -78,8 +78,10 @@ struct Fused2Args {
   int k_begin, k_end;  // level-(l+1) quad rows produced by this launch
   int n_super;         // CTA super-strips
   int n_ctas;
-  unsigned long long* tail_counter;  // [0] tickets, [1] CTAs done (self-resetting), or null
-  int tail_chunk;                    // level-(l+1) rows per dynamic chunk
+  unsigned long long* tail_counter;  // [0] claimed tail rows, [1] CTAs done, [2] edge tickets
+                                     // (self-resetting), or null
+  int tail_chunk;                    // level-(l+1) rows per dynamic chunk (the smallest, when guided)
+  int guided;                        // tail claims: guided self-scheduling (1) or fixed chunks (0)
   // work space (f2_work_space on the host), in cost units of one interior
   // level-(l+1) row: [0, edge_cost) = the n_edge checked units of unit_rows rows
   // at the image top / bottom (`top` / `bot` rows per super-strip), each
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
   const int lane = threadIdx.x % kLaneCount;
   const int cta = blockIdx.x;
   if (cta >= a.n_ctas) return;
-  __shared__ unsigned long long s_ticket;
+  __shared__ long long s_claim[2];  // dynamic item: kind/offset, size
 
   // shared memory: per-warp TMA rings | their mbarriers | LL ring | its mbarriers [slot][warp]
   const size_t ring0_bytes = static_cast<size_t>(WARPS) * STAGES * Src::kStageElems * sizeof(T);
@@ -415,23 +417,29 @@ __global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
         f = a.edge_cost + c0 + a.rows_in;
         if (k0 >= k1) continue;
       }
-    } else {  // next dynamic tail chunk (interior rows)
-      int j;
-      if (a.tail_counter != nullptr) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_ticket = atomicAdd(a.tail_counter, 1ull);
-        __syncthreads();
-        j = static_cast<int>(min(s_ticket, static_cast<unsigned long long>(a.n_dyn)));
-      } else {
-        j = a.n_dyn;
+    } else {  // next dynamic item: an edge unit, then guided interior ranges
+      if (a.tail_counter == nullptr) break;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const long long e = a.dyn_edges > 0 ? static_cast<long long>(atomicAdd(a.tail_counter + 2, 1ull)) : 0;
+        if (e < a.dyn_edges) {
+          s_claim[0] = -1 - e;  // edge unit e
+          s_claim[1] = 0;
+        } else {
+          int64_t sz = 0;
+          s_claim[0] = claim_guided(a.tail_counter, a.total - a.static_end, a.tail_chunk, a.n_ctas, a.guided != 0, &sz);
+          s_claim[1] = sz;
+        }
       }
-      if (j >= a.n_dyn) break;
-      if (j < a.dyn_edges) {  // edge unit j: its cost range, taken whole by this CTA
-        f = j * a.unit_cost;
+      __syncthreads();
+      const long long c = s_claim[0];
+      if (c < 0) {  // edge unit: its cost range, taken whole by this CTA
+        f = static_cast<int>(-1 - c) * a.unit_cost;
         f_end = f + 1;
       } else {
-        f = a.static_end + (j - a.dyn_edges) * a.tail_chunk;
-        f_end = min(a.total, f + a.tail_chunk);
+        f = a.static_end + static_cast<int>(c);
+        if (f >= a.total) break;
+        f_end = min(a.total, f + static_cast<int>(s_claim[1]));
       }
       continue;
     }
@@ -539,6 +547,7 @@ __global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
     if (atomicAdd(a.tail_counter + 1, 1ull) == static_cast<unsigned long long>(a.n_ctas) - 1) {
       a.tail_counter[0] = 0;
       a.tail_counter[1] = 0;
+      a.tail_counter[2] = 0;
       __threadfence();
     }
   }

@@ -36,7 +36,8 @@ struct FusedLaunch {
   long long* dbg;         // per-warp timing records (b2dwt_debug_*), usually null
   unsigned long long* tail_counter;  // zeroed device counter for the dynamic tail, or null
   int static_frac;        // share of the work split statically (1/1024)
-  int tail_rows;          // rows per dynamic tail chunk
+  int tail_rows;          // rows per dynamic tail chunk (the smallest, when guided)
+  int guided;             // guided self-scheduling of the tail (0: fixed chunks)
   int strip_align;        // strip start / width alignment in quads (>= 2)
   int full_rows;
   bool pdl;               // launch with programmatic stream serialization
@@ -63,6 +64,7 @@ struct Fused2Launch {
   unsigned long long* tail_counter;
   int static_frac;
   int tail_rows1;
+  int guided;
   int edge_rows1;  // level-(l+1) rows per checked unit at the image top / bottom
   int min_rows1;
   bool pdl;

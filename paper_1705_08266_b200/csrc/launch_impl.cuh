@@ -212,6 +212,7 @@ cudaError_t launch(const FusedLaunch& r) {
   a.tail_counter = rows_per_cta >= 64 ? r.tail_counter : nullptr;
   a.static_frac = std::min(1024, std::max(0, r.static_frac));
   a.tail_chunk = static_cast<int>(std::max<int64_t>(4, std::min<int64_t>(r.tail_rows, rows_per_cta / 8))) * 8;
+  a.guided = r.guided;
 
   CUtensorMap maps[4];
   memset(maps, 0, sizeof(maps));

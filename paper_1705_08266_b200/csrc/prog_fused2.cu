@@ -97,6 +97,7 @@ cudaError_t launch(const Fused2Launch& r) {
   const int64_t per_cta = total / a.n_ctas;
   a.tail_counter = per_cta >= 64 ? r.tail_counter : nullptr;
   a.tail_chunk = static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(r.tail_rows1, per_cta / 4)));
+  a.guided = r.guided;
   f2_work_space(a, std::min(1024, std::max(0, r.static_frac)), r.edge_rows1);
 
   EncodeTiledFn enc = encode_fn();

@@ -70,10 +70,12 @@ struct StreamArgs {
   int n_warps;              // CTAs sharing the (item, super-strip, row) space
   int edge_cost;            // cost of an image-edge strip row, in 1/8 of an interior row
   long long* dbg;           // optional per-warp timing record (debug builds of the split), or null
-  unsigned long long* tail_counter;  // [0] tail chunk tickets, [1] warps done (null: fully static split);
-                                     // the last warp out resets both, so the slot is reusable
+  unsigned long long* tail_counter;  // [0] claimed tail units, [1] CTAs done, [2] (fused kernel) edge
+                                     // tickets; null: fully static split.  The last CTA out resets them,
+                                     // so the slot is reusable
   int static_frac;          // share of the cost split statically, in 1/1024
-  int tail_chunk;           // cost units per dynamic tail chunk
+  int tail_chunk;           // cost units per dynamic tail chunk (the smallest, when guided)
+  int guided;               // tail claims: guided self-scheduling (1) or fixed chunks (0)
 };
 
 __host__ __device__ constexpr int cmod(int x, int m) { return ((x % m) + m) % m; }
@@ -913,6 +915,31 @@ __device__ __forceinline__ void steady_chunk(Pipe& pipe, Src& src, int t, const 
 }
 
 // ---------------------------------------------------------------------------
+// Dynamic tail: the next range of the cost space [0, span) past the static
+// share, claimed by one thread for its CTA.  Guided self-scheduling: half of a
+// fair share of what remains (remaining / (2 x CTAs)), at least `min_chunk`
+// units, so early claims are long (few cone re-reads and ring restarts) and
+// the last ones short (balance).  guided == 0: fixed min_chunk tickets.
+// Returns the claim's offset, or `span` when nothing is left.
+__device__ __forceinline__ int64_t claim_guided(unsigned long long* pos, int64_t span, int64_t min_chunk,
+                                                int n_ctas, bool guided, int64_t* size) {
+  int64_t sz = min_chunk;
+  if (guided) {
+    // size from a plain (possibly stale) read, then ONE fetch-add: a CAS loop
+    // serialised the ~444 CTAs that finish their static shares together
+    // (measured 4x slower); a stale size only makes that claim a little long
+    const int64_t rem = span - static_cast<int64_t>(*reinterpret_cast<volatile unsigned long long*>(pos));
+    if (rem <= 0) return span;
+    const int64_t g = rem / (2 * static_cast<int64_t>(n_ctas));
+    sz = g > min_chunk ? g : min_chunk;
+  }
+  const int64_t f = static_cast<int64_t>(atomicAdd(pos, static_cast<unsigned long long>(sz)));
+  if (f >= span) return span;
+  *size = sz < span - f ? sz : span - f;
+  return f;
+}
+
+// ---------------------------------------------------------------------------
 // The kernel.
 //   P        program structure (programs.inc)
 //   T        float | double
@@ -950,7 +977,7 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
   if (cta >= a.n_warps) return;  // (n_warps counts CTAs here) block-uniform
   const long long clk0 = clock64();
   int dbg_rows = 0, dbg_edge_rows = 0;
-  __shared__ unsigned long long s_ticket;
+  __shared__ long long s_claim[2];  // dynamic tail: offset, size
 
   // Work unit = (item, SUPER-strip of WARPS adjacent strips, row range); warp k
   // of the CTA takes strip WARPS*ss + k over the same rows.  Adjacent strips'
@@ -1126,20 +1153,24 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
     src.finish();
   }
     if (static_end >= total) break;
-    // the CTA's warps claim the next tail chunk together (same rows, adjacent strips)
+    // the CTA's warps claim the next tail range together (same rows, adjacent strips)
     __syncthreads();
-    if (threadIdx.x == 0) s_ticket = atomicAdd(a.tail_counter, 1ull);
+    if (threadIdx.x == 0) {
+      int64_t sz = 0;
+      s_claim[0] = claim_guided(a.tail_counter, total - static_end, a.tail_chunk, a.n_warps, a.guided != 0, &sz);
+      s_claim[1] = sz;
+    }
     __syncthreads();
-    const unsigned long long j = s_ticket;
-    f = static_end + static_cast<int64_t>(j) * a.tail_chunk;
+    f = static_end + s_claim[0];
     if (f >= total) break;
-    f_end = min(total, f + static_cast<int64_t>(a.tail_chunk));
+    f_end = min(total, f + static_cast<int64_t>(s_claim[1]));
   }
   if (a.tail_counter != nullptr && threadIdx.x == 0) {
     // every CTA has drawn its last ticket before it gets here
     if (atomicAdd(a.tail_counter + 1, 1ull) == static_cast<unsigned long long>(a.n_warps) - 1) {
       a.tail_counter[0] = 0;
       a.tail_counter[1] = 0;
+      a.tail_counter[2] = 0;
       __threadfence();
     }
   }
