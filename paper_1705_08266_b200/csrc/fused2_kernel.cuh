@@ -83,16 +83,25 @@ struct Fused2Args {
   int tail_chunk;                    // level-(l+1) rows per dynamic chunk (the smallest, when guided)
   int guided;                        // tail claims: guided self-scheduling (1) or fixed chunks (0)
   // work space (f2_work_space on the host), in cost units of one interior
-  // level-(l+1) row: [0, edge_cost) = the n_edge checked units of unit_rows rows
-  // at the image top / bottom (`top` / `bot` rows per super-strip), each
-  // costing unit_cost; then [edge_cost, total) = interior rows [ki0, ki0 +
-  // rows_in) of every super-strip.  [static_begin, static_end) is split evenly
-  // over the CTAs (a unit goes to the CTA whose share holds its first cost
-  // unit); with a tail counter the edge units are the first dynamic items
-  // (dyn_edges) and the interior past static_end follows in tail chunks.
+  // level-(l+1) row.  The rows near the image top / bottom (`top` / `bot` per
+  // super-strip) need the checked path and run as n_edge units of unit_rows
+  // rows, each costing unit_cost; the interior rows [ki0, ki0 + rows_in) of
+  // every super-strip are the rest.
+  //  * small launch (no tail counter), space 0: [0, edge_cost) = the edge
+  //    units, [edge_cost, total) = the interior super-strip by super-strip;
+  //    [0, total) is split evenly over the CTAs (a unit goes to the CTA whose
+  //    share holds its first cost unit);
+  //  * large launch: static space 1 = the first s_rows interior rows of every
+  //    super-strip, split evenly over the first static_ctas CTAs -- a whole
+  //    multiple of n_super, so every share lies inside ONE super-strip (one
+  //    cone fill per CTA); then the dynamic queue: the edge units first
+  //    (dyn_edges tickets), then space 2 = the remaining d_rows rows of every
+  //    super-strip ([0, n_dyn_rows)) in guided claims.
   int top, bot, ki0, rows_in, n_edge, unit_cost, edge_cost;
   int unit_rows, units_top, units_bot;  // an edge band is cut into units of unit_rows rows
-  int total, static_begin, static_end, dyn_edges, n_dyn;
+  int total;                                      // small launch: size of space 0
+  int s_rows, d_rows, static_ctas, n_dyn_rows;   // large launch: spaces 1 and 2
+  int dyn_edges;
 };
 
 // Host: fill the work-space fields of `a` (its k range, n_super, n_ctas,
@@ -128,19 +137,18 @@ inline void f2_work_space(Fused2Args<T>& a, int static_frac, int edge_rows = kF2
   a.unit_cost = 4 * a.unit_rows;  // checked ticks at both levels plus both cones (measured ~4x an interior row)
   a.edge_cost = a.n_edge * a.unit_cost;
   a.total = a.edge_cost + a.n_super * a.rows_in;
+  a.s_rows = a.d_rows = a.static_ctas = a.n_dyn_rows = a.dyn_edges = 0;
   if (a.tail_counter != nullptr) {
-    // large launch: the slow edge units go to whichever CTAs finish their
-    // static share first (head of the dynamic list)
-    a.static_begin = a.edge_cost;
-    a.static_end = a.edge_cost + static_cast<int>(static_cast<int64_t>(a.total - a.edge_cost) * static_frac / 1024);
+    // large launch: whole super-strip slices for the static CTAs (C3 levels
+    // 0+1: 444 CTAs = 12 per super-strip); the slow edge units go to whichever
+    // CTAs finish their static share first (head of the dynamic list)
+    const int per_super = a.n_ctas / a.n_super;
+    a.static_ctas = per_super >= 1 ? per_super * a.n_super : a.n_ctas;
+    a.s_rows = static_cast<int>(static_cast<int64_t>(a.rows_in) * static_frac * a.static_ctas / (1024 * int64_t{a.n_ctas}));
+    a.d_rows = a.rows_in - a.s_rows;
+    a.n_dyn_rows = a.n_super * a.d_rows;
     a.dyn_edges = a.n_edge;
-  } else {
-    // small launch: everything static, edge units weighted into the split
-    a.static_begin = 0;
-    a.static_end = a.total;
-    a.dyn_edges = 0;
   }
-  a.n_dyn = a.dyn_edges + (a.total - a.static_end + a.tail_chunk - 1) / a.tail_chunk;
 }
 
 // Level-l sink: HL/LH/HH straight to HBM (8-B vectors), LL into the ring.
@@ -372,9 +380,19 @@ __global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
 
   const int rows1 = a.rows / 2, cols1 = a.cols / 2;
   // work space: see Fused2Args / f2_work_space
-  const int64_t span = a.static_end - a.static_begin;
-  int f = a.static_begin + static_cast<int>(span * cta / a.n_ctas);
-  int f_end = a.static_begin + static_cast<int>(span * (cta + 1) / a.n_ctas);
+  int space, f = 0, f_end = 0;  // the current range [f, f_end) of work space `space`
+  if (a.tail_counter == nullptr) {
+    space = 0;
+    f = static_cast<int>(int64_t{a.total} * cta / a.n_ctas);
+    f_end = static_cast<int>(int64_t{a.total} * (cta + 1) / a.n_ctas);
+  } else {
+    space = 1;
+    if (cta < a.static_ctas) {
+      const int64_t span = int64_t{a.n_super} * a.s_rows;
+      f = static_cast<int>(span * cta / a.static_ctas);
+      f_end = static_cast<int>(span * (cta + 1) / a.static_ctas);
+    }
+  }
 
   F2Level1<P, T, kStrict> l1;
   l1.bars = ll_bars;
@@ -390,7 +408,7 @@ __global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
     // next unit: super-strip `sup`, level-(l+1) rows [k0, k1) (CTA-uniform)
     int sup, k0, k1;
     if (f < f_end) {
-      if (f < a.edge_cost) {  // edge units: this CTA's if their first cost unit lies in [f, f_end)
+      if (space == 0 && f < a.edge_cost) {  // edge units: this CTA's if their first cost unit lies in [f, f_end)
         const int e = (f + a.unit_cost - 1) / a.unit_cost;  // first unit starting at or after f
         if (e >= a.n_edge || e * a.unit_cost >= f_end) {  // none: continue with the interior rows
           f = min(a.edge_cost, f_end);
@@ -408,13 +426,16 @@ __global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
           k0 = a.k_end - a.bot + (eb - sup * a.units_bot) * a.unit_rows;
           k1 = min(a.k_end, k0 + a.unit_rows);
         }
-      } else {  // interior rows
-        const int g = f - a.edge_cost;
-        sup = g / a.rows_in;
-        const int c0 = sup * a.rows_in;
-        k0 = a.ki0 + (g - c0);
-        k1 = a.ki0 + min(a.rows_in, f_end - a.edge_cost - c0);
-        f = a.edge_cost + c0 + a.rows_in;
+      } else {  // interior rows: row space 0 (after the edges), 1 (static) or 2 (dynamic)
+        const int ib = space == 0 ? a.edge_cost : 0;
+        const int rps = space == 0 ? a.rows_in : space == 1 ? a.s_rows : a.d_rows;
+        const int kb = space == 2 ? a.ki0 + a.s_rows : a.ki0;
+        const int g = f - ib;
+        sup = g / rps;
+        const int c0 = sup * rps;
+        k0 = kb + (g - c0);
+        k1 = kb + min(rps, f_end - ib - c0);
+        f = ib + c0 + rps;
         if (k0 >= k1) continue;
       }
     } else {  // next dynamic item: an edge unit, then guided interior ranges
@@ -427,19 +448,21 @@ __global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
           s_claim[1] = 0;
         } else {
           int64_t sz = 0;
-          s_claim[0] = claim_guided(a.tail_counter, a.total - a.static_end, a.tail_chunk, a.n_ctas, a.guided != 0, &sz);
+          s_claim[0] = claim_guided(a.tail_counter, a.n_dyn_rows, a.tail_chunk, a.n_ctas, a.guided != 0, &sz);
           s_claim[1] = sz;
         }
       }
       __syncthreads();
       const long long c = s_claim[0];
-      if (c < 0) {  // edge unit: its cost range, taken whole by this CTA
+      if (c < 0) {  // edge unit: its cost range in space 0, taken whole by this CTA
+        space = 0;
         f = static_cast<int>(-1 - c) * a.unit_cost;
         f_end = f + 1;
       } else {
-        f = a.static_end + static_cast<int>(c);
-        if (f >= a.total) break;
-        f_end = min(a.total, f + static_cast<int>(s_claim[1]));
+        space = 2;
+        f = static_cast<int>(c);
+        if (f >= a.n_dyn_rows) break;
+        f_end = min(a.n_dyn_rows, f + static_cast<int>(s_claim[1]));
       }
       continue;
     }

@@ -19,8 +19,10 @@ def timed(g, reps=30):
     return s.elapsed_time(e) / reps
 
 
-for fast in (True, False):
-    for fuse in (True, False):
+# MODES: comma list of fast:fuse pairs, e.g. "1:1,0:1" (default: all four)
+modes = [tuple(bool(int(v)) for v in m.split(":")) for m in os.environ.get("MODES", "1:1,1:0,0:1,0:0").split(",")]
+for fast, fuse in modes:
+    if True:
         tr = Transform(build_scheme("non-separable-split", CDF97), "single", fast=fast, fuse=fuse)
         g = tr.capture_dwt(x, levels)
         ms = timed(g)
