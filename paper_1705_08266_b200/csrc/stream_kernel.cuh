@@ -948,6 +948,9 @@ __device__ __forceinline__ int64_t claim_guided(unsigned long long* pos, int64_t
 //   kTma     fill the ring with TMA (requires 16 B pitches) instead of cp.async
 // f32: cap registers at 168/thread so 3 CTAs (12 warps) fit per SM; without
 // the hint ptxas spends ~200 and only 2 CTAs fit.
+#ifndef B2DWT_WARP_CLAIM
+#define B2DWT_WARP_CLAIM 1
+#endif
 #ifndef B2DWT_UNROLL
 #define B2DWT_UNROLL 1
 #endif
@@ -1027,6 +1030,7 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
+  int wk = warp;  // which strip of the current super-strip this warp runs
 #pragma unroll 1
   for (;;) {
 #pragma unroll 1
@@ -1055,9 +1059,9 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
     const int r0 = static_cast<int>((f - c0 + wr - 1) / wr);
     const int r1 = static_cast<int>(min(static_cast<int64_t>(rows_out), (f_end - c0 + wr - 1) / wr));
     f = c0 + wr * rows_out;  // next super-strip
-    int strip = sup * WARPS + warp;
+    int strip = sup * WARPS + wk;
     if (span) {  // global strip -> (item, strip)
-      const int64_t g = static_cast<int64_t>(sup) * WARPS + warp;
+      const int64_t g = static_cast<int64_t>(sup) * WARPS + wk;
       if (g >= n_gstrips) continue;
       b = static_cast<int>(g / a.n_strips);
       strip = static_cast<int>(g - static_cast<int64_t>(b) * a.n_strips);
@@ -1153,6 +1157,22 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
     src.finish();
   }
     if (static_end >= total) break;
+#if B2DWT_WARP_CLAIM
+    {
+      // every warp draws its own tail tickets: ticket t = strip t % WARPS of
+      // fixed chunk t / WARPS (a CTA-wide claim parked the CTA's early warps at
+      // a barrier until its slowest one finished: ~10% of the stall samples of
+      // cdf97 convolution, profiles/r02_ncu_conv97_counters.txt)
+      unsigned long long t = 0;
+      if (lane == 0) t = atomicAdd(a.tail_counter, 1ull);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      wk = static_cast<int>(t % WARPS);
+      f = static_end + static_cast<int64_t>(t / WARPS) * a.tail_chunk;
+      if (f >= total) break;
+      f_end = min(total, f + static_cast<int64_t>(a.tail_chunk));
+      continue;
+    }
+#endif
     // the CTA's warps claim the next tail range together (same rows, adjacent strips)
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1165,6 +1185,9 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
     if (f >= total) break;
     f_end = min(total, f + static_cast<int64_t>(s_claim[1]));
   }
+#if B2DWT_WARP_CLAIM
+  if (a.tail_counter != nullptr) __syncthreads();  // every warp of the CTA has drawn its last ticket
+#endif
   if (a.tail_counter != nullptr && threadIdx.x == 0) {
     // every CTA has drawn its last ticket before it gets here
     if (atomicAdd(a.tail_counter + 1, 1ull) == static_cast<unsigned long long>(a.n_warps) - 1) {
