@@ -483,6 +483,9 @@ def run_c3(args):
                 "alg_bytes_rule": "SURVEY 8(d): 8 B/px of every level the launch processes",
                 "compulsory_bytes": l0_compulsory,
                 "frac_compulsory": l0_compulsory / (l0_ms * 1e-3) / 1e9 / peak,
+                "note": ("a fused pair's frac can exceed 1: the 8 B/px rule counts level l's LL write and level "
+                         "l+1's re-read, which the fused kernel keeps in shared memory; frac_compulsory counts "
+                         "only the bytes it must move") if g0b > g0a else None,
                 "launch_ms": l0_ms,
                 "timing": "event nodes around the first launch group inside the captured graph, mean over K replays",
             },
