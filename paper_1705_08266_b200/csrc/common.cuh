@@ -35,6 +35,20 @@ B2DWT_HD constexpr int col_parity(int c) { return c & 1; }
 // Component index actually read at quad index i for a component of phase
 // `parity` and length cs: whole-sample symmetric extension in pixel
 // coordinates (engine.py:55-92).  Periodic, so tiny sizes fold repeatedly.
+// Row address base + n * ldb (ldb: pitch in bytes) for the fused kernel's
+// sinks.  Written as int64 arithmetic there, the compiler kept the operands'
+// sign words in registers and emitted a 64 x 64 multiply (4 instructions per
+// store address); as unsigned 32 x 32 -> 64 the loop got shorter (711 vs 739
+// instructions) but slower.  Measured on C3 (tools/ab_lib.sh, same box):
+// levels 0+1 406.6 -> 405.7 us fast, 445 -> 429 us strict with this form;
+// 420 / 460 us unsigned.  (The stream kernel's int64 form already compiles to
+// one IMAD.WIDE with the base as addend and keeps it.)
+__device__ __forceinline__ char* row_addr(const void* base, int n, int ldb) {
+  unsigned long long r;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(n), "r"(ldb), "l"(base));
+  return reinterpret_cast<char*>(r);
+}
+
 __device__ __forceinline__ int reflect(int i, int parity, int cs) {
   const int size = 2 * cs;  // >= 2
   const int period = 2 * size - 2;

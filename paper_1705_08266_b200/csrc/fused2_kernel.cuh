@@ -74,6 +74,7 @@ struct Fused2Args {
   // level-(l+1) LL/HL/LH/HH
   T* out1_pl[4];
   int64_t out1_ld[4];
+  int out1_ldb[4];  // out1_ld in bytes (the host checks that it fits)
   int rows, cols;      // level-l quad grid
   int k_begin, k_end;  // level-(l+1) quad rows produced by this launch
   int n_super;         // CTA super-strips
@@ -186,7 +187,7 @@ struct F2Sink0 {
     const bool vok = in_range && full && vec;
 #pragma unroll
     for (int c = 1; c < 4; ++c) {
-      char* p = base[c] + static_cast<int64_t>(n) * ldb[c];
+      char* p = row_addr(base[c], n, ldb[c]);
       st_pred<T, 2>(p, v[c], vok);
       if (kScalar && any_scalar) {
         if (in_range && !(full && vec)) {
@@ -223,7 +224,13 @@ struct F2Sink1 {
   __device__ __forceinline__ void store(const T (&v)[4][1], int n, bool in_range) {
     if (in_range && lane_ok) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) a->out1_pl[c][static_cast<int64_t>(n) * a->out1_ld[c] + m_lane] = v[c][0];
+      for (int c = 0; c < 4; ++c) {
+        const T* p = reinterpret_cast<const T*>(row_addr(a->out1_pl[c], n, a->out1_ldb[c])) + m_lane;
+        if constexpr (sizeof(T) == 4)
+          asm volatile("st.global.f32 [%0], %1;\n" ::"l"(p), "f"(v[c][0]) : "memory");
+        else
+          asm volatile("st.global.f64 [%0], %1;\n" ::"l"(p), "d"(v[c][0]) : "memory");
+      }
     }
   }
 };

@@ -82,6 +82,7 @@ cudaError_t launch(const Fused2Launch& r) {
     a.out_ld[c] = r.out0_ld[c];
     a.out1_pl[c] = static_cast<T*>(r.out1_pl[c]);
     a.out1_ld[c] = r.out1_ld[c];
+    a.out1_ldb[c] = static_cast<int>(r.out1_ld[c] * static_cast<int64_t>(sizeof(T)));
   }
   a.out_row0 = 0;
   a.rows = r.rows;
