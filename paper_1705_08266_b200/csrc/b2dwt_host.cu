@@ -696,7 +696,11 @@ int run_fused2_pair(const b2dwt_plan_s& p, const void* in, int64_t in_ld, int64_
   r.tail_rows1 = f2_tail;
   r.guided = guided_tail(true);
   r.edge_rows1 = f2_edge;
-  r.min_rows1 = std::max(8, min_rows() / 2);
+  static const int f2_min_rows = [] {  // fewest level-(l+1) rows per CTA (0: from min_rows())
+    const char* e = std::getenv("B2DWT_F2_MIN_ROWS");
+    return e ? std::atoi(e) : 0;
+  }();
+  r.min_rows1 = f2_min_rows > 0 ? f2_min_rows : std::max(8, min_rows() / 2);
   r.pdl = split_param(4) != 0;
   r.stream = stream;
   // footprint-bounded launches, as run_fused: row bands of <= 1 GiB of input

@@ -96,7 +96,13 @@ cudaError_t launch(const Fused2Launch& r) {
   const int64_t min_rows = std::max(1, r.min_rows1);
   a.n_ctas = static_cast<int>(std::max<int64_t>(1, std::min(resident, (total + min_rows - 1) / min_rows)));
   const int64_t per_cta = total / a.n_ctas;
-  a.tail_counter = per_cta >= 64 ? r.tail_counter : nullptr;
+  // dynamic tail only when a CTA's share is long (small launches: all static,
+  // edge units weighted in); B2DWT_F2_DYN_MIN overrides the 64-row threshold
+  static const int dyn_min = [] {
+    const char* e = std::getenv("B2DWT_F2_DYN_MIN");
+    return e ? std::atoi(e) : 64;
+  }();
+  a.tail_counter = per_cta >= dyn_min ? r.tail_counter : nullptr;
   a.tail_chunk = static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(r.tail_rows1, per_cta / 4)));
   a.guided = r.guided;
   f2_work_space(a, std::min(1024, std::max(0, r.static_frac)), r.edge_rows1);
