@@ -197,7 +197,9 @@ unsigned long long* tail_counter_slot(cudaStream_t stream) {
 // Guided self-scheduling of the dynamic tail (claim_guided, stream_kernel.cuh).
 // Measured: the two-level fused kernel gains (C3 levels 0+1 427 -> 408 us with a
 // 768/1024 static share), the stream kernel does not (C4 +1.6%, C5 -1%), so the
-// defaults differ.  B2DWT_GUIDED / B2DWT_F2_GUIDED override (0 / 1).
+// defaults differ.  The value k > 0 sizes a claim as remaining / (k x CTAs); 0
+// means fixed chunks.  B2DWT_GUIDED / B2DWT_F2_GUIDED override (defaults 0 / 1: for the
+// fused kernel a full fair share, tools/guided_sweep.sh: levels 0+1 403 -> 392 us vs k = 2).
 int guided_tail(bool fused2) {
   static const int v[2] = {[] {
                              const char* e = std::getenv("B2DWT_GUIDED");
@@ -680,7 +682,7 @@ int run_fused2_pair(const b2dwt_plan_s& p, const void* in, int64_t in_ld, int64_
   // work split of the fused kernel: a unit re-reads the cones of BOTH levels
   // (~14 level-l rows), so its dynamic tail chunks are longer than the stream
   // kernel's.  B2DWT_F2_STATIC_FRAC / B2DWT_F2_TAIL_ROWS override.
-  static const int f2_static = [] {  // measured on C3 (tools/tail_sweep.sh): 768 with guided claims
+  static const int f2_static = [] {  // measured on C3 (tools/guided_sweep.sh): 768-832 with k = 1 claims
     const char* e = std::getenv("B2DWT_F2_STATIC_FRAC");
     return e ? std::atoi(e) : 768;
   }();

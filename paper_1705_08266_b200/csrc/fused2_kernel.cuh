@@ -82,7 +82,7 @@ struct Fused2Args {
   unsigned long long* tail_counter;  // [0] claimed tail rows, [1] CTAs done, [2] edge tickets
                                      // (self-resetting), or null
   int tail_chunk;                    // level-(l+1) rows per dynamic chunk (the smallest, when guided)
-  int guided;                        // tail claims: guided self-scheduling (1) or fixed chunks (0)
+  int guided;                        // tail claims: guided, a 1/k share of the rest (k > 0), or fixed chunks (0)
   // work space (f2_work_space on the host), in cost units of one interior
   // level-(l+1) row.  The rows near the image top / bottom (`top` / `bot` per
   // super-strip) need the checked path and run as n_edge units of unit_rows
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(4 * kLaneCount, B2DWT_F2_MIN_CTAS)
           s_claim[1] = 0;
         } else {
           int64_t sz = 0;
-          s_claim[0] = claim_guided(a.tail_counter, a.n_dyn_rows, a.tail_chunk, a.n_ctas, a.guided != 0, &sz);
+          s_claim[0] = claim_guided(a.tail_counter, a.n_dyn_rows, a.tail_chunk, a.n_ctas, a.guided, &sz);
           s_claim[1] = sz;
         }
       }

@@ -37,7 +37,7 @@ struct FusedLaunch {
   unsigned long long* tail_counter;  // zeroed device counter for the dynamic tail, or null
   int static_frac;        // share of the work split statically (1/1024)
   int tail_rows;          // rows per dynamic tail chunk (the smallest, when guided)
-  int guided;             // guided self-scheduling of the tail (0: fixed chunks)
+  int guided;             // guided self-scheduling of the tail: claims of remaining / (k x CTAs), k = guided (0: fixed chunks)
   int strip_align;        // strip start / width alignment in quads (>= 2)
   int full_rows;
   bool pdl;               // launch with programmatic stream serialization

@@ -75,7 +75,7 @@ struct StreamArgs {
                                      // so the slot is reusable
   int static_frac;          // share of the cost split statically, in 1/1024
   int tail_chunk;           // cost units per dynamic tail chunk (the smallest, when guided)
-  int guided;               // tail claims: guided self-scheduling (1) or fixed chunks (0)
+  int guided;               // tail claims: guided, a 1/k share of the rest (k > 0), or fixed chunks (0)
 };
 
 __host__ __device__ constexpr int cmod(int x, int m) { return ((x % m) + m) % m; }
@@ -916,21 +916,21 @@ __device__ __forceinline__ void steady_chunk(Pipe& pipe, Src& src, int t, const 
 
 // ---------------------------------------------------------------------------
 // Dynamic tail: the next range of the cost space [0, span) past the static
-// share, claimed by one thread for its CTA.  Guided self-scheduling: half of a
-// fair share of what remains (remaining / (2 x CTAs)), at least `min_chunk`
-// units, so early claims are long (few cone re-reads and ring restarts) and
-// the last ones short (balance).  guided == 0: fixed min_chunk tickets.
-// Returns the claim's offset, or `span` when nothing is left.
+// share, claimed by one thread for its CTA.  Guided self-scheduling (guided =
+// k > 0): a k-th of a fair share of what remains (remaining / (k x CTAs)), at
+// least `min_chunk` units, so early claims are long (few cone re-reads and ring
+// restarts) and the last ones short (balance).  guided == 0: fixed min_chunk
+// tickets.  Returns the claim's offset, or `span` when nothing is left.
 __device__ __forceinline__ int64_t claim_guided(unsigned long long* pos, int64_t span, int64_t min_chunk,
-                                                int n_ctas, bool guided, int64_t* size) {
+                                                int n_ctas, int guided, int64_t* size) {
   int64_t sz = min_chunk;
-  if (guided) {
+  if (guided > 0) {
     // size from a plain (possibly stale) read, then ONE fetch-add: a CAS loop
     // serialised the ~444 CTAs that finish their static shares together
     // (measured 4x slower); a stale size only makes that claim a little long
     const int64_t rem = span - static_cast<int64_t>(*reinterpret_cast<volatile unsigned long long*>(pos));
     if (rem <= 0) return span;
-    const int64_t g = rem / (2 * static_cast<int64_t>(n_ctas));
+    const int64_t g = rem / (static_cast<int64_t>(guided) * n_ctas);
     sz = g > min_chunk ? g : min_chunk;
   }
   const int64_t f = static_cast<int64_t>(atomicAdd(pos, static_cast<unsigned long long>(sz)));
@@ -1177,7 +1177,7 @@ __global__ void __launch_bounds__(WARPS* kLaneCount, (sizeof(T) == 4 ? B2DWT_MIN
     __syncthreads();
     if (threadIdx.x == 0) {
       int64_t sz = 0;
-      s_claim[0] = claim_guided(a.tail_counter, total - static_end, a.tail_chunk, a.n_warps, a.guided != 0, &sz);
+      s_claim[0] = claim_guided(a.tail_counter, total - static_end, a.tail_chunk, a.n_warps, a.guided, &sz);
       s_claim[1] = sz;
     }
     __syncthreads();
