@@ -57,6 +57,11 @@ constexpr int kF2Ring = B2DWT_F2_RING;  // ring slots (level-(l+1) rows)
 constexpr int kF2J = 116;               // ring columns (level-(l+1) quads)
 constexpr int kF2W1 = 28;               // level-(l+1) columns stored per warp
 constexpr int kF2Edge = 8;      // level-(l+1) rows at the image top / bottom run as checked units
+// level-(l+1) steps of a steady chunk in pairs: one neighbour wait per two
+// steps (F2Level1::step2)
+#ifndef B2DWT_F2_PAIR
+#define B2DWT_F2_PAIR 1  // C3 strict levels 0+1 415 -> 408 us, fast unchanged (tools/ab_lib.sh)
+#endif
 
 template <class T>
 struct Fused2Args {
@@ -287,6 +292,39 @@ struct F2Level1 {
     ++u;
   }
 
+  // Paired steps (B2DWT_F2_PAIR): the first of two consecutive steps only
+  // signals its slot; the second signals, waits for the neighbours ONCE (their
+  // arrival for the later step orders their ring writes for both: arrive is a
+  // release, the wait an acquire) and reads both rows.  Slot reuse stays safe
+  // with 5 slots: a warp's waits now lag its reads by one step, and the
+  // rewrite of a slot is still >= 2 waited steps behind its last read.
+  __device__ __forceinline__ void arrive_only() {
+    const unsigned s = u % kF2Ring;
+    mbar_arrive(bars + (s * 4) * 8 + warp * 8);
+    ++u;
+  }
+  template <int PHA, int PHB, int HEDGE, class Args>
+  __device__ __forceinline__ void step2(int t1a, const Args& a) {
+    const unsigned s = u % kF2Ring, par = (u / kF2Ring) & 1u;
+    const unsigned sp = (u + kF2Ring - 1) % kF2Ring;
+    const unsigned b = bars + (s * 4) * 8;
+    mbar_arrive(b + warp * 8);
+    if (warp > 0) mbar_wait_sa(b + (warp - 1) * 8, par);
+    if (warp < 3) mbar_wait_sa(b + (warp + 1) * 8, par);
+    __syncwarp();
+    T ra[4][1], rb[4][1];
+    const unsigned pa = rd + sp * (kF2J * 4) * static_cast<unsigned>(sizeof(T));
+    const unsigned pb = rd + s * (kF2J * 4) * static_cast<unsigned>(sizeof(T));
+    static_assert(sizeof(T) == 4, "paired steps: f32 only");
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=f"(ra[0][0]), "=f"(ra[1][0]), "=f"(ra[2][0]), "=f"(ra[3][0]) : "r"(pa) : "memory");
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=f"(rb[0][0]), "=f"(rb[1][0]), "=f"(rb[2][0]), "=f"(rb[3][0]) : "r"(pb) : "memory");
+    ++u;
+    pipe.template tick<PHA, false, HEDGE>(ra, t1a, cx, a, sink);
+    pipe.template tick<PHB, false, HEDGE>(rb, t1a + 1, cx, a, sink);
+  }
+
   // Unchecked level-(l+1) tick at compile-time phase PH1.
   template <int PH1, int HEDGE, class Args>
   __device__ __forceinline__ void step(int t1, const Args& a) {
@@ -330,7 +368,17 @@ __device__ __forceinline__ void f2_steady_chunk(Pipe0& pipe0, Src& src, F2Level1
     pipe0.template tick<i, false, HEDGE>(row, t + i, cx0, a, sink0);
     if constexpr (((i - kD0) % 2 + 2) % 2 == 1) {  // LL row t + i - kD0 is odd: a quad row is complete
       sink0.slot = static_cast<int>((l1.u + 1) % kF2Ring);
-      l1.template step<cmod((i - kD0 - 1) / 2, kP), HEDGE>((t + i - kD0 - 1) / 2, a);
+      // j-th level-(l+1) step of the chunk (kD0 fixes which ticks complete a row)
+      constexpr int j = (i - (((kD0 + 1) % 2 + 2) % 2)) / 2;
+      constexpr int n_steps = static_cast<int>(sizeof...(I)) / 2;
+      if constexpr (B2DWT_F2_PAIR && sizeof(T) == 4 && n_steps % 2 == 0 && j % 2 == 0) {
+        l1.arrive_only();
+      } else if constexpr (B2DWT_F2_PAIR && sizeof(T) == 4 && n_steps % 2 == 0) {
+        l1.template step2<cmod((i - kD0 - 1) / 2 - 1, kP), cmod((i - kD0 - 1) / 2, kP), HEDGE>(
+            (t + i - kD0 - 1) / 2 - 1, a);
+      } else {
+        l1.template step<cmod((i - kD0 - 1) / 2, kP), HEDGE>((t + i - kD0 - 1) / 2, a);
+      }
     }
   };
   if constexpr (kNest) src.advance_if_due(a, m, m, m, m);  // t % period == 0: the only possible stage switch
