@@ -682,9 +682,12 @@ int run_fused2_pair(const b2dwt_plan_s& p, const void* in, int64_t in_ld, int64_
   // work split of the fused kernel: a unit re-reads the cones of BOTH levels
   // (~14 level-l rows), so its dynamic tail chunks are longer than the stream
   // kernel's.  B2DWT_F2_STATIC_FRAC / B2DWT_F2_TAIL_ROWS override.
-  static const int f2_static = [] {  // measured on C3 (tools/guided_sweep.sh): 768-832 with k = 1 claims
+  // static share, measured on C3 with k = 1 claims (tools/guided_sweep.sh,
+  // tools/sf_ab.sh): 832/1024 for fast plans (768: +0.4%), 768 for strict ones
+  // (832: +1.1%, the slower pipeline wants the longer dynamic tail)
+  static const int f2_static_env = [] {
     const char* e = std::getenv("B2DWT_F2_STATIC_FRAC");
-    return e ? std::atoi(e) : 768;
+    return e ? std::atoi(e) : -1;
   }();
   static const int f2_tail = [] {
     const char* e = std::getenv("B2DWT_F2_TAIL_ROWS");
@@ -694,6 +697,7 @@ int run_fused2_pair(const b2dwt_plan_s& p, const void* in, int64_t in_ld, int64_
     const char* e = std::getenv("B2DWT_F2_EDGE_ROWS");
     return e ? std::atoi(e) : 8;
   }();
+  const int f2_static = f2_static_env >= 0 ? f2_static_env : (r.strict ? 768 : 832);
   r.static_frac = f2_static;
   r.tail_rows1 = f2_tail;
   r.guided = guided_tail(true);
